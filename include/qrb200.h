@@ -1,0 +1,160 @@
+/*
+ * qrb200 -- C ABI of the B200-native (sm_100a) FP64 blocked Householder QR and
+ * multi-slice least-squares solve.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `oocqr` (Python).  The reference exposes the path as two Python functions
+ * re-exported from pkg/src/oocqr/__init__.py:9-23:
+ *
+ *   factorize(a, config, factors_dir, geometry_hash="")   task_engine.py:606-641
+ *   solve(factors, b_mat, config, out_dir)                task_engine.py:644-685
+ *
+ * whose work is dispatched per tile by `_run_kernel` (task_engine.py:287-317)
+ * to six numpy/numba kernels (kernels.py:296-455).  The Python mirror in
+ * paper_1907_01891_b200/task_engine.py keeps those two signatures and calls
+ * this library through ctypes; each entry point below names the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *   - all matrices are column-major float64 with an explicit leading dimension
+ *     (the reference's on-disk tile order, tile_store.py:25-30);
+ *   - return value: 0 = ok; > 0 = singular triangular factor, the value is
+ *     1 + the global column the reference would report (kernels.py:423-426
+ *     visited bottom-up in tiles of `report_block`, task_engine.py:246-253);
+ *     < 0 = error code (QRB_E*), message via qrb_last_error();
+ *   - host buffers are borrowed for the duration of a call; device memory owned
+ *     by a handle is freed by qrb_destroy; `stream` arguments are cudaStream_t
+ *     passed as void* (0 = legacy default stream);
+ *   - a handle is single-caller; calls return after the device work finished
+ *     unless documented as stream-ordered ("_op_" entry points).
+ */
+#ifndef QRB200_H
+#define QRB200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define QRB_API __attribute__((visibility("default")))
+#else
+#define QRB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QRB_OK 0
+#define QRB_EARG (-1)
+#define QRB_ECUDA (-2)
+#define QRB_ENOMEM (-3)
+#define QRB_ENONFINITE (-4)
+#define QRB_ESTATE (-5)
+#define QRB_EUNSUPPORTED (-6)
+
+typedef struct qrb_handle qrb_handle;
+
+/* Timing/accounting of one call; mirrors the reference RunReport
+ * (task_engine.py:136-181) with device-side (CUDA event) times. */
+typedef struct qrb_report {
+  double total_ms;     /* whole call, CUDA events on the handle stream        */
+  double panel_ms;     /* panel factorization (geqr2 + larft) share           */
+  double update_ms;    /* trailing / Q^T block-reflector updates             */
+  double trsm_ms;      /* back substitution                                   */
+  double h2d_ms;       /* host -> device copies inside the call               */
+  double d2h_ms;       /* device -> host copies inside the call               */
+  double flops;        /* algorithmic flops (2mn^2 - 2n^3/3, or 4mn - n^2 per slice) */
+  int64_t kernel_launches; /* kernels this library launched for the call     */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} qrb_report;
+
+/* library */
+QRB_API int qrb_version(void);
+QRB_API const char* qrb_last_error(void);
+QRB_API int qrb_device_count(int* count);
+QRB_API int qrb_set_device(int device);
+
+/* ---- handle API (drop-in for factorize / solve) ------------------------ */
+
+/* Allocate an m x n (m >= n) matrix on `device` with panel width nb
+ * (reference EngineConfig.inner_block, task_engine.py:77-121).
+ * Replaces: factorize's store setup (task_engine.py:614-628). */
+QRB_API int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out);
+QRB_API int qrb_destroy(qrb_handle* h);
+
+/* Copy columns [col0, col0+ncols) of A in/out (column-major, leading dim ld).
+ * After qrb_factorize, qrb_get_matrix returns the factored storage: R on and
+ * above the diagonal, Householder vectors (implicit unit diagonal) below --
+ * the reference `factored` store convention (kernels.py:6-14).
+ * Replaces: TiledMatrix load_tile/store_tile staging (tile_store.py:181-209). */
+QRB_API int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src, int64_t ld,
+                   int src_on_device);
+QRB_API int qrb_get_matrix(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
+                   int dst_on_device);
+
+/* In-place blocked Householder QR of the handle's matrix.
+ * Replaces: factorize -> execute(gen_factorization_tasks) (task_engine.py:606-641,
+ * 187-217) and kernels comp_dense_qr / comp_td_qr / apply_left_qt_* (kernels.py:296-405).
+ * Returns QRB_ENONFINITE if A holds NaN/Inf (KernelInputError, kernels.py:305-306). */
+QRB_API int qrb_factorize(qrb_handle* h, qrb_report* rep);
+
+/* Persisted-factor interop: tau (n) and the per-panel T factors
+ * (nb x nb each, panel k at T + k*nb*ldt... stored as an nb x (npanels*nb) matrix). */
+QRB_API int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt);
+QRB_API int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t ldt);
+
+/* X = R^-1 (Q^T B)[0:n] for nrhs right-hand sides; resid[j] = ||(Q^T B)[n:m, j]||_2
+ * (= ||A x_j - b_j||_2; may be NULL).  B is m x nrhs (ldb), X is n x nrhs (ldx).
+ * `on_device` = 1 when B/X/resid are device pointers.  report_block = the tile
+ * size whose bottom-up order decides which singular column is reported.
+ * Replaces: solve -> execute(gen_solve_tasks) (task_engine.py:644-685, 220-254)
+ * with apply_left_qt_* / gemm_nn_mo / trsm_lunn (kernels.py:324-455). */
+QRB_API int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double* X, int64_t ldx,
+              double* resid, int on_device, int64_t report_block, qrb_report* rep);
+
+/* Diagonal of R (n values, host).  Used for the singularity rule. */
+QRB_API int qrb_get_rdiag(qrb_handle* h, double* diag);
+
+/* ---- stream-ordered device-pointer operators ----------------------------
+ * Used by the multi-GPU driver (one process per GPU, NCCL broadcast of each
+ * panel between calls) and by the parity tests.  All pointers are device
+ * pointers; work is enqueued on `stream` and not synchronized. */
+
+/* Householder QR of an m x w panel (w <= 128) in place + its T factor (w x w,
+ * upper).  Replaces comp_dense_qr's panel loop + T builder (kernels.py:80-169). */
+QRB_API int qrb_op_panel(double* panel, int64_t ldp, int64_t m, int64_t w, double* tau, double* T,
+                 int64_t ldt, void* stream);
+
+/* C <- Q^T C with Q = I - V T V^T, V (m x w, unit lower, stored in place under
+ * R) and T (w x w).  Replaces apply_left_qt_dense (kernels.py:324-341). */
+QRB_API int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
+                    int64_t ldt, double* C, int64_t ldc, int64_t nc, void* stream);
+
+/* C <- C - A B (A m x k, B k x n).  Replaces gemm_nn_mo (kernels.py:442-455). */
+QRB_API int qrb_op_gemm_nn_sub(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                       int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream);
+
+/* C (M x N) = A^T B with A (K x M), B (K x N); K split into `splits` ranges
+ * summed in a fixed order.  mask_a / mask_b: treat that operand as a unit-lower
+ * Householder block (upper triangle 0, diagonal 1).  Building block of the
+ * W = V^T C step of apply_left_qt_* (kernels.py:337, 400). */
+QRB_API int qrb_op_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                           int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int mask_a,
+                           int mask_b, void* stream);
+
+/* B <- upper(R)^-1 B for an n x n upper-triangular R (block size nb).
+ * Replaces trsm_lunn (kernels.py:408-439) for a whole triangular factor. */
+QRB_API int qrb_op_trsm_upper(const double* R, int64_t ldr, int64_t n, int nb, double* B, int64_t ldb,
+                      int64_t nrhs, void* stream);
+
+/* Kernels launched by this library since load (gpu_launches accounting). */
+QRB_API int64_t qrb_launch_count(void);
+
+/* Release all library workspaces of the current device. */
+QRB_API int qrb_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QRB200_H */

@@ -1,0 +1,26 @@
+// Internal C++ interface of the DMMA GEMM family (see gemm_dmma.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qrb {
+
+enum { GEMM_EPI_STORE = 0, GEMM_EPI_SUB = 1 };
+
+// out(M x N) [+ split z * split_stride] = Aview^T * Bview, Aview K x M, Bview K x N.
+// K is split into `splits` contiguous ranges, each written to its own slice.
+int gemm_tn(const MatView& a_km, const MatView& b, double* out, int64_t ldo, int64_t split_stride,
+            int M, int N, int K, int splits, int mask_a, int mask_b, cudaStream_t stream);
+
+// as gemm_tn; *used = number of K slices actually written (<= splits)
+int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ldo,
+                  int64_t split_stride, int M, int N, int K, int splits, int mask_a, int mask_b,
+                  cudaStream_t stream, int* used);
+
+// out(M x N) (=|-=) Aview * Bview, Aview M x K, Bview K x N.
+int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int M, int N, int K,
+            int epi, int mask_a, cudaStream_t stream);
+
+int gemm_pick_splits(int M, int N, int K, int max_splits);
+int gemm_sm_count();
+
+}  // namespace qrb

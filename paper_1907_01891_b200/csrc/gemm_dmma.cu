@@ -1,0 +1,425 @@
+// FP64 tensor-core GEMM family for the blocked Householder QR (sm_100a).
+//
+// The compact-WY trailing update of a panel (reference: kernels.py:315-319,
+// 332-340, 375-380, 396-404 -- W = V^T C ; Z = T^T W ; C -= V Z) and the
+// off-diagonal back-substitution update (reference gemm_nn_mo, kernels.py:442-455)
+// are all dense FP64 contractions.  They run here on the FP64 tensor pipe
+// (DMMA.8x8x4 via mma.sync.m8n8k4.f64) fed by TMA:
+//
+//   * one producer warp streams 16-deep K slices of both operands with
+//     cp.async.bulk.tensor (128-byte swizzle) into a 4-stage shared-memory ring
+//     guarded by mbarriers (full: TMA transaction count, empty: consumer warps);
+//   * eight consumer warps load conflict-free 16-byte fragments
+//     (ld.shared.v2.f64) and issue DMMA with register accumulators (tcgen05 /
+//     TMEM have no FP64 kind on Blackwell, so this is the FP64 tensor path);
+//   * the epilogue either stores the tile or subtracts it from C in place.
+//
+// Operand conventions (all matrices column-major, views are MatView):
+//   A_KMAJOR = true  : op(A) = Aview^T, Aview is K x M (rows = K)   [W = V^T C]
+//   A_KMAJOR = false : op(A) = Aview,   Aview is M x K (rows = M)   [C -= V W]
+//   B is always a K x N view (rows = K).
+// A view flagged "unit lower" (a Householder block V stored in place under R)
+// is read with its upper triangle as zeros and its diagonal as ones -- the
+// same implicit-unit-diagonal convention as the reference's _unit_lower
+// (kernels.py:286-290).  TMA zero-fills everything outside a view, so ragged
+// M/N/K edges need no padding.
+#include "common.cuh"
+#include "gemm.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+namespace qrb {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 16;
+constexpr int STAGES = 4;
+constexpr int CONSUMER_WARPS = 8;
+constexpr int THREADS = (CONSUMER_WARPS + 1) * 32;
+
+struct GemmArgs {
+  int M, N, K;
+  int k_per_split;
+  double* out;
+  int64_t ldo;
+  int64_t split_stride;
+  int mask_a, mask_b;
+  int group_m;
+};
+
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return static_cast<uint32_t>(row * 128 + (((chunk ^ (row & 7)) & 7) << 4));
+}
+
+// unit-lower-trapezoid masking of a pair of consecutive view rows (r, r+1) at view column c
+__device__ __forceinline__ void mask_pair(double2& v, int r, int c) {
+  if (r <= c) v.x = (r == c) ? 1.0 : 0.0;
+  if (r + 1 <= c) v.y = (r + 1 == c) ? 1.0 : 0.0;
+}
+
+template <bool A_KMAJOR, int BN, bool MASK_A, bool MASK_B>
+__device__ __forceinline__ void consume_stage(double (&acc)[4][BN / 16][2], const uint8_t* sA,
+                                              const uint8_t* sB, int m0, int n0, int g, int q,
+                                              int kg0, int mg0, int ng0) {
+  constexpr int NT = BN / 16;
+#pragma unroll
+  for (int kc = 0; kc < BK; kc += 8) {
+    double2 b[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int row = n0 + nt * 8 + g;
+      b[nt] = *reinterpret_cast<const double2*>(sB + swz(row, (kc >> 1) + q));
+      if constexpr (MASK_B) mask_pair(b[nt], kg0 + kc + 2 * q, ng0 + row);
+    }
+    if constexpr (A_KMAJOR) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int row = m0 + mt * 8 + g;
+        double2 a = *reinterpret_cast<const double2*>(sA + swz(row, (kc >> 1) + q));
+        if constexpr (MASK_A) mask_pair(a, kg0 + kc + 2 * q, mg0 + row);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a.x, b[nt].x);
+          dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a.y, b[nt].y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const int k = kc + 2 * q + p;
+#pragma unroll
+        for (int mp = 0; mp < 2; ++mp) {
+          const int m = m0 + mp * 16 + 2 * g;  // even row; pair (m, m+1)
+          double2 a = *reinterpret_cast<const double2*>(sA + (m >> 4) * 2048 + swz(k, (m & 15) >> 1));
+          if constexpr (MASK_A) mask_pair(a, mg0 + m, kg0 + k);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double bv = p ? b[nt].y : b[nt].x;
+            dmma_8x8x4(acc[mp * 2 + 0][nt][0], acc[mp * 2 + 0][nt][1], a.x, bv);
+            dmma_8x8x4(acc[mp * 2 + 1][nt][0], acc[mp * 2 + 1][nt][1], a.y, bv);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool A_KMAJOR, int BN, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, const GemmArgs args) {
+  constexpr int NT = BN / 16;
+  constexpr uint32_t A_BYTES = BM * BK * 8;
+  constexpr uint32_t B_BYTES = BN * BK * 8;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // tile rasterization: groups of group_m M-tiles sweep the N-tiles together
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + BN - 1) / BN;
+  const int tile = blockIdx.x;
+  const int per_group = args.group_m * num_n;
+  const int first_m = (tile / per_group) * args.group_m;
+  const int gsize = min(num_m - first_m, args.group_m);
+  const int local = tile % per_group;
+  const int m_tile = first_m + local % gsize;
+  const int n_tile = local / gsize;
+
+  const int k_begin = blockIdx.z * args.k_per_split;
+  const int k_end = min(args.K, k_begin + args.k_per_split);
+  const int num_k = (k_end - k_begin + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {
+    // ---------------- producer warp: TMA ----------------
+    if (lane == 0 && num_k > 0) {
+      prefetch_tmap(&mapA);
+      prefetch_tmap(&mapB);
+      for (int kt = 0; kt < num_k; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+        uint8_t* sA = smem + s * STAGE_BYTES;
+        uint8_t* sB = sA + A_BYTES;
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        const int k = k_begin + kt * BK;
+        if constexpr (A_KMAJOR) {
+          tma_load_2d(sA, &mapA, k, m_tile * BM, &full[s]);
+        } else {
+#pragma unroll
+          for (int mb = 0; mb < BM / 16; ++mb)
+            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+        }
+        tma_load_2d(sB, &mapB, k, n_tile * BN, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps: DMMA ----------------
+  const int g = lane >> 2;
+  const int q = lane & 3;
+  const int m0 = (warp & 3) * 32;
+  const int n0 = (warp >> 2) * (BN / 2);
+  const int mg0 = m_tile * BM;
+  const int ng0 = n_tile * BN;
+
+  double acc[4][NT][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < num_k; ++kt) {
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    const uint8_t* sA = smem + s * STAGE_BYTES;
+    const uint8_t* sB = sA + A_BYTES;
+    const int kg0 = k_begin + kt * BK;
+    bool ma = false, mb = false;
+    if (args.mask_a) {
+      ma = A_KMAJOR ? (kg0 <= mg0 + BM - 1) : (mg0 <= kg0 + BK - 1);
+    }
+    if (args.mask_b) mb = (kg0 <= ng0 + BN - 1);
+    if (ma || mb) {
+      if (ma && mb)
+        consume_stage<A_KMAJOR, BN, true, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else if (ma)
+        consume_stage<A_KMAJOR, BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else
+        consume_stage<A_KMAJOR, BN, false, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+    } else {
+      consume_stage<A_KMAJOR, BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue ----------------
+  double* out = args.out + static_cast<int64_t>(blockIdx.z) * args.split_stride;
+  const int64_t ldo = args.ldo;
+  if constexpr (A_KMAJOR) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int m = mg0 + m0 + mt * 8 + g;
+      if (m >= args.M) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = ng0 + n0 + nt * 8 + 2 * q;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (n + e < args.N) {
+            double* p = out + m + static_cast<int64_t>(n + e) * ldo;
+            if constexpr (EPI == GEMM_EPI_SUB)
+              *p -= acc[mt][nt][e];
+            else
+              *p = acc[mt][nt][e];
+          }
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int mp = 0; mp < 2; ++mp) {
+      const int m = mg0 + m0 + mp * 16 + 2 * g;
+      if (m >= args.M) continue;
+      const bool pair = (m + 1 < args.M);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = ng0 + n0 + nt * 8 + 2 * q;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (n + e >= args.N) continue;
+          double* p = out + m + static_cast<int64_t>(n + e) * ldo;
+          const double v0 = acc[mp * 2 + 0][nt][e];
+          const double v1 = acc[mp * 2 + 1][nt][e];
+          if (pair) {
+            double2* p2 = reinterpret_cast<double2*>(p);
+            if constexpr (EPI == GEMM_EPI_SUB) {
+              double2 c = *p2;
+              c.x -= v0;
+              c.y -= v1;
+              *p2 = c;
+            } else {
+              *p2 = make_double2(v0, v1);
+            }
+          } else {
+            if constexpr (EPI == GEMM_EPI_SUB)
+              *p -= v0;
+            else
+              *p = v0;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encoder() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult qres;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres) ==
+            cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return QRB_ERR_CUDA;
+  }
+  return QRB_OK;
+}
+
+int make_map(CUtensorMap* map, const MatView& v, uint32_t box_rows, uint32_t box_cols) {
+  QRB_TRY(get_encoder());
+  if (v.rows < 1 || v.cols < 1) {
+    set_last_error("make_map: empty view");
+    return QRB_ERR_ARG;
+  }
+  if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) != 0 || (v.ld & 1) != 0) {
+    set_last_error("make_map: view base must be 16-byte aligned and ld even");
+    return QRB_ERR_ARG;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(v.rows), static_cast<cuuint64_t>(v.cols)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(v.ld) * 8};
+  cuuint32_t box[2] = {box_rows, box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, v.ptr, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return QRB_ERR_CUDA;
+  }
+  return QRB_OK;
+}
+
+template <bool A_KMAJOR, int BN, int EPI>
+int launch(const MatView& a, const MatView& b, double* out, int64_t ldo, int64_t split_stride,
+           int M, int N, int K, int splits, int mask_a, int mask_b, cudaStream_t stream,
+           int* used = nullptr) {
+  constexpr int SMEM = STAGES * (BM * BK * 8 + BN * BK * 8) + 2 * STAGES * 8 + 1024;
+  static bool configured = false;
+  if (!configured) {
+    QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_dmma_kernel<A_KMAJOR, BN, EPI>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    configured = true;
+  }
+  CUtensorMap ma, mb;
+  if (A_KMAJOR)
+    QRB_TRY(make_map(&ma, a, BK, BM));
+  else
+    QRB_TRY(make_map(&ma, a, 16, BK));
+  QRB_TRY(make_map(&mb, b, BK, BN));
+  GemmArgs args;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  int kps = (K + splits - 1) / splits;
+  kps = ((kps + BK - 1) / BK) * BK;
+  args.k_per_split = kps;
+  args.out = out;
+  args.ldo = ldo;
+  args.split_stride = split_stride;
+  args.mask_a = mask_a;
+  args.mask_b = mask_b;
+  args.group_m = 16;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int nsplit = (K + kps - 1) / kps;
+  if (used) *used = nsplit;
+  dim3 grid(num_m * num_n, 1, nsplit);
+  gemm_dmma_kernel<A_KMAJOR, BN, EPI><<<grid, THREADS, SMEM, stream>>>(ma, mb, args);
+  QRB_CUDA_TRY(cudaGetLastError());
+  return QRB_OK;
+}
+
+}  // namespace
+
+int gemm_sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// number of K splits for a long-K (TN) product so that the tile grid fills
+// the machine with little wave quantization
+int gemm_pick_splits(int M, int N, int K, int max_splits) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
+  const int slots = 2 * gemm_sm_count();
+  const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= std::min(max_splits, kmax); ++s) {
+    const long units = static_cast<long>(tiles) * s;
+    const long waves = (units + slots - 1) / slots;
+    const double eff = static_cast<double>(units) / static_cast<double>(waves * slots);
+    // prefer fewer splits unless a split count is clearly better
+    if (eff > best_eff + 0.03) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+int gemm_tn(const MatView& a_km, const MatView& b, double* out, int64_t ldo, int64_t split_stride,
+            int M, int N, int K, int splits, int mask_a, int mask_b, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
+  return launch<true, 64, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,
+                                          mask_a, mask_b, stream);
+}
+
+int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ldo,
+                  int64_t split_stride, int M, int N, int K, int splits, int mask_a, int mask_b,
+                  cudaStream_t stream, int* used) {
+  *used = 0;
+  if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
+  return launch<true, 64, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,
+                                          mask_a, mask_b, stream, used);
+}
+
+int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int M, int N, int K,
+            int epi, int mask_a, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0 || (ldo & 1) != 0) {
+    set_last_error("gemm_nn: output must be 16-byte aligned with even ld");
+    return QRB_ERR_ARG;
+  }
+  if (epi == GEMM_EPI_SUB)
+    return launch<false, 64, GEMM_EPI_SUB>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
+  return launch<false, 64, GEMM_EPI_STORE>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
+}
+
+}  // namespace qrb

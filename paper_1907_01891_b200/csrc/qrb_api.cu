@@ -1,0 +1,683 @@
+// C ABI of the B200 FP64 QR library (include/qrb200.h): device handle,
+// right-looking blocked Householder QR driver, block-reflector application
+// and the multi-slice least-squares solve.
+//
+// Reference path being replaced (pkg/src/oocqr):
+//   factorize  task_engine.py:606-641  -> qrb_factorize
+//   solve      task_engine.py:644-685  -> qrb_solve
+//   kernels    kernels.py:296-455      -> panel_factor / apply_qt / trsm below
+// The reference orders the work as a left-looking tile DAG to minimise disk
+// writes (task_engine.py:187-254); with the matrix resident in HBM the
+// B200-native order is right-looking by panels of nb columns, every trailing
+// update being two large DMMA GEMMs.
+#include "common.cuh"
+#include "gemm.h"
+#include "panel.h"
+
+#include "../../include/qrb200.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace qrb {
+
+static thread_local std::string t_last_error;
+void set_last_error(const std::string& msg) { t_last_error = msg; }
+
+// ---------------------------------------------------------------------------
+// grow-only device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need, cudaStream_t st) {
+    if (need <= bytes) return QRB_OK;
+    if (p) {
+      QRB_CUDA_TRY(cudaStreamSynchronize(st));
+      QRB_CUDA_TRY(cudaFree(p));
+      p = nullptr;
+      bytes = 0;
+    }
+    if (cudaMalloc(&p, need) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      set_last_error("cudaMalloc of " + std::to_string(need) + " bytes failed");
+      return QRB_ERR_NOMEM;
+    }
+    bytes = need;
+    return QRB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(p); }
+};
+
+struct Workspace {
+  DevBuf part, bar, G, Ti, W, W2, Wparts;
+  void release() {
+    part.release();
+    bar.release();
+    G.release();
+    Ti.release();
+    W.release();
+    W2.release();
+    Wparts.release();
+  }
+};
+
+static std::atomic<int64_t> g_launches{0};
+
+static Workspace& device_workspace() {
+  static Workspace ws[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return ws[dev & 63];
+}
+
+static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+// C <- (I - V T^T V^T) C   i.e. C <- Q^T C,  V m x w unit lower (in place under R)
+static int apply_qt(const MatView& V, const double* T, int64_t ldt, const MatView& C,
+                    Workspace& ws, cudaStream_t st) {
+  const int m = static_cast<int>(V.rows);
+  const int w = static_cast<int>(V.cols);
+  const int nc = static_cast<int>(C.cols);
+  if (nc <= 0 || w <= 0 || m <= 0) return QRB_OK;
+  const int64_t ldw = even(w);
+  QRB_TRY(ws.W.ensure(sizeof(double) * ldw * nc, st));
+  QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));
+  const int64_t per_split = ldw * nc;
+  const int max_splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(32) << 20) / per_split)));
+  const int splits = gemm_pick_splits(w, nc, m, max_splits);
+  if (splits > 1) {
+    QRB_TRY(ws.Wparts.ensure(sizeof(double) * per_split * splits, st));
+    int used = 0;
+    QRB_TRY(gemm_tn_split(V, C, ws.Wparts.d(), ldw, per_split, w, nc, m, splits, 1, 0, st, &used));
+    QRB_TRY(reduce_splits(ws.Wparts.d(), per_split, used, w, nc, ldw, ws.W.d(), ldw, st));
+    g_launches += 2;
+  } else {
+    QRB_TRY(gemm_tn(V, C, ws.W.d(), ldw, 0, w, nc, m, 1, 1, 0, st));
+    g_launches += 1;
+  }
+  // W2 = T^T W
+  MatView Tv{const_cast<double*>(T), w, w, ldt};
+  MatView Wv{ws.W.d(), w, nc, ldw};
+  QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
+  // C -= V W2
+  MatView W2v{ws.W2.d(), w, nc, ldw};
+  QRB_TRY(gemm_nn(V, W2v, C.ptr, C.ld, m, nc, w, GEMM_EPI_SUB, 1, st));
+  g_launches += 2;
+  return QRB_OK;
+}
+
+// Householder QR of an m x w panel (w <= 128) in place, tau[w], T (w x w, ldt)
+static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
+                        cudaStream_t st) {
+  const int m = static_cast<int>(panel.rows);
+  const int pw = static_cast<int>(panel.cols);
+  if (pw <= 0) return QRB_OK;
+  if (m < pw) {
+    set_last_error("panel rows < width");
+    return QRB_ERR_ARG;
+  }
+  const int ldg = 128;
+  QRB_TRY(ws.G.ensure(sizeof(double) * ldg * 128, st));
+  QRB_TRY(ws.Ti.ensure(sizeof(double) * 128 * 128, st));
+  QRB_TRY(ws.bar.ensure(64, st));
+  PanelPlan pl = panel_plan(m, pw);
+  QRB_TRY(ws.part.ensure(sizeof(double) * ((size_t)(pl.P + 1) * (128 + 2) + 64), st));
+  unsigned int* bar = static_cast<unsigned int*>(ws.bar.p);
+  if (pl.ib >= pw) {
+    QRB_TRY(panel_factor(panel, pl.P, pl.R, tau, ws.G.d(), ldg, ws.part.d(), bar, st));
+    QRB_TRY(build_t(ws.G.d(), ldg, tau, pw, T, static_cast<int>(ldt), st));
+    g_launches += 3;  // memset + panel + build_t
+    return QRB_OK;
+  }
+  const int ib = pl.ib;
+  for (int i0 = 0; i0 < pw; i0 += ib) {
+    const int w = std::min(ib, pw - i0);
+    const int mi = m - i0;
+    PanelPlan pi = panel_plan(mi, w);
+    MatView sub = panel.sub(i0, i0, mi, w);
+    QRB_TRY(panel_factor(sub, pi.P, pi.R, tau + i0, ws.G.d(), ldg, ws.part.d(), bar, st));
+    g_launches += 2;
+    if (i0 + w < pw) {
+      QRB_TRY(build_t(ws.G.d(), ldg, tau + i0, w, ws.Ti.d(), 128, st));
+      g_launches += 1;
+      QRB_TRY(apply_qt(sub, ws.Ti.d(), 128, panel.sub(i0, i0 + w, mi, pw - i0 - w), ws, st));
+    }
+  }
+  // Gram matrix of the whole panel, then T
+  const int64_t per = int64_t(ldg) * pw;
+  const int splits = gemm_pick_splits(pw, pw, m, 64);
+  if (splits > 1) {
+    QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+    int used = 0;
+    QRB_TRY(gemm_tn_split(panel, panel, ws.Wparts.d(), ldg, per, pw, pw, m, splits, 1, 1, st,
+                          &used));
+    QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, pw, pw, ldg, ws.G.d(), ldg, st));
+    g_launches += 2;
+  } else {
+    QRB_TRY(gemm_tn(panel, panel, ws.G.d(), ldg, 0, pw, pw, m, 1, 1, 1, st));
+    g_launches += 1;
+  }
+  QRB_TRY(build_t(ws.G.d(), ldg, tau, pw, T, static_cast<int>(ldt), st));
+  g_launches += 1;
+  return QRB_OK;
+}
+
+// B (n x nrhs) <- upper(R)^-1 B using precomputed inverses of the nb x nb diagonal blocks
+static int trsm_upper(const MatView& R, const double* Rinv, int nb, const MatView& B,
+                      cudaStream_t st) {
+  const int n = static_cast<int>(R.rows);
+  const int nrhs = static_cast<int>(B.cols);
+  if (n <= 0 || nrhs <= 0) return QRB_OK;
+  const int nblk = (n + nb - 1) / nb;
+  for (int k = nblk - 1; k >= 0; --k) {
+    const int i0 = k * nb;
+    const int bs = std::min(nb, n - i0);
+    MatView Ri{const_cast<double*>(Rinv) + (int64_t)k * nb * nb, bs, bs, nb};
+    MatView Yk = B.sub(i0, 0, bs, nrhs);
+    QRB_TRY(gemm_nn(Ri, Yk, Yk.ptr, Yk.ld, bs, nrhs, bs, GEMM_EPI_STORE, 0, st));
+    g_launches += 1;
+    if (i0 > 0) {
+      MatView Rk = R.sub(0, i0, i0, bs);
+      QRB_TRY(gemm_nn(Rk, Yk, B.ptr, B.ld, i0, nrhs, bs, GEMM_EPI_SUB, 0, st));
+      g_launches += 1;
+    }
+  }
+  return QRB_OK;
+}
+
+__global__ void nonfinite_kernel(const double* A, int64_t lda, int64_t m, int64_t n, int* flag) {
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / m, r = idx - c * m;
+    if (!isfinite(A[r + c * lda])) {
+      *flag = 1;
+      return;
+    }
+  }
+}
+
+// first singular column in the reference's bottom-up tile order (kernels.py:423-426,
+// task_engine.py:246-253): diagonal tiles visited from the last one up, first
+// |d| < 1e-300 (or NaN) inside the first bad tile met.
+static int64_t singular_column(const std::vector<double>& diag, int64_t block) {
+  const int64_t n = static_cast<int64_t>(diag.size());
+  if (block <= 0) block = n > 0 ? n : 1;
+  const int64_t ntiles = (n + block - 1) / block;
+  for (int64_t t = ntiles - 1; t >= 0; --t) {
+    const int64_t e = std::min(n, (t + 1) * block);
+    for (int64_t i = t * block; i < e; ++i) {
+      if (!(std::fabs(diag[i]) >= 1e-300)) return i;
+    }
+  }
+  return -1;
+}
+
+}  // namespace qrb
+
+using namespace qrb;
+
+struct qrb_handle {
+  int device = 0;
+  int64_t m = 0, n = 0, lda = 0;
+  int nb = 128;
+  int npanels = 0;
+  double* A = nullptr;
+  double* tau = nullptr;
+  double* T = nullptr;     // nb x (npanels * nb), ld = nb
+  double* Rinv = nullptr;  // npanels blocks of nb x nb
+  bool factored = false;
+  bool rinv_ready = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  DevBuf Bw;  // solve work buffer
+  DevBuf resid;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void clear_report(qrb_report* rep) {
+  if (rep) std::memset(rep, 0, sizeof(*rep));
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+int ensure_rinv(qrb_handle* h) {
+  if (h->rinv_ready) return QRB_OK;
+  QRB_TRY(trtri_blocks(h->A, h->lda, static_cast<int>(h->n), h->nb, h->Rinv, h->stream));
+  g_launches += 1;
+  h->rinv_ready = true;
+  return QRB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qrb_version(void) { return 100; }
+
+const char* qrb_last_error(void) { return t_last_error.c_str(); }
+
+int qrb_device_count(int* count) {
+  if (!count) return QRB_EARG;
+  QRB_CUDA_TRY(cudaGetDeviceCount(count));
+  return QRB_OK;
+}
+
+int qrb_set_device(int device) {
+  QRB_CUDA_TRY(cudaSetDevice(device));
+  return QRB_OK;
+}
+
+int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
+  if (!out || m < 1 || n < 1 || m < n || nb < 16 || nb > 128 || (nb % 16) != 0) {
+    set_last_error("qrb_create: need m >= n >= 1 and nb in {16, 32, ..., 128}");
+    return QRB_EARG;
+  }
+  if (m > (int64_t(1) << 31) - 1024 || n > (int64_t(1) << 31) - 1024) {
+    set_last_error("qrb_create: dimensions exceed int32 TMA coordinates");
+    return QRB_EARG;
+  }
+  *out = nullptr;
+  QRB_CUDA_TRY(cudaSetDevice(device));
+  qrb_handle* h = new qrb_handle();
+  h->device = device;
+  h->m = m;
+  h->n = n;
+  h->lda = (m + 31) & ~int64_t(31);
+  h->nb = nb;
+  h->npanels = static_cast<int>((n + nb - 1) / nb);
+  auto fail = [&](const char* what) {
+    set_last_error(std::string("qrb_create: ") + what);
+    qrb_destroy(h);
+    return QRB_ENOMEM;
+  };
+  if (cudaMalloc(&h->A, sizeof(double) * h->lda * n) != cudaSuccess) return fail("matrix alloc");
+  if (cudaMalloc(&h->tau, sizeof(double) * n) != cudaSuccess) return fail("tau alloc");
+  if (cudaMalloc(&h->T, sizeof(double) * nb * nb * h->npanels) != cudaSuccess)
+    return fail("T alloc");
+  if (cudaMalloc(&h->Rinv, sizeof(double) * nb * nb * h->npanels) != cudaSuccess)
+    return fail("Rinv alloc");
+  cudaGetLastError();
+  QRB_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  QRB_CUDA_TRY(cudaEventCreate(&h->ev0));
+  QRB_CUDA_TRY(cudaEventCreate(&h->ev1));
+  QRB_CUDA_TRY(cudaEventCreate(&h->ev2));
+  QRB_CUDA_TRY(cudaMemsetAsync(h->A, 0, sizeof(double) * h->lda * n, h->stream));
+  QRB_CUDA_TRY(cudaMemsetAsync(h->T, 0, sizeof(double) * nb * nb * h->npanels, h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  *out = h;
+  return QRB_OK;
+}
+
+int qrb_destroy(qrb_handle* h) {
+  if (!h) return QRB_OK;
+  DeviceGuard g(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->A) cudaFree(h->A);
+  if (h->tau) cudaFree(h->tau);
+  if (h->T) cudaFree(h->T);
+  if (h->Rinv) cudaFree(h->Rinv);
+  h->Bw.release();
+  h->resid.release();
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev2) cudaEventDestroy(h->ev2);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return QRB_OK;
+}
+
+int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src, int64_t ld,
+                   int src_on_device) {
+  if (!h || !src || col0 < 0 || ncols < 0 || col0 + ncols > h->n || ld < h->m) {
+    set_last_error("qrb_set_matrix: bad arguments");
+    return QRB_EARG;
+  }
+  DeviceGuard g(h->device);
+  if (ncols == 0) return QRB_OK;
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double), src,
+                                 ld * sizeof(double), h->m * sizeof(double), ncols,
+                                 src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->factored = false;
+  h->rinv_ready = false;
+  return QRB_OK;
+}
+
+int qrb_get_matrix(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
+                   int dst_on_device) {
+  if (!h || !dst || col0 < 0 || ncols < 0 || col0 + ncols > h->n || ld < h->m) {
+    set_last_error("qrb_get_matrix: bad arguments");
+    return QRB_EARG;
+  }
+  DeviceGuard g(h->device);
+  if (ncols == 0) return QRB_OK;
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(dst, ld * sizeof(double), h->A + col0 * h->lda,
+                                 h->lda * sizeof(double), h->m * sizeof(double), ncols,
+                                 dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return QRB_OK;
+}
+
+int qrb_factorize(qrb_handle* h, qrb_report* rep) {
+  clear_report(rep);
+  if (!h) return QRB_EARG;
+  DeviceGuard g(h->device);
+  Workspace& ws = device_workspace();
+  const int64_t launches0 = g_launches.load();
+  cudaStream_t st = h->stream;
+  // non-finite input -> KernelInputError (kernels.py:305-306)
+  {
+    QRB_TRY(ws.bar.ensure(64, st));
+    int* flag = static_cast<int*>(ws.bar.p) + 4;
+    QRB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A, h->lda, h->m, h->n, flag);
+    QRB_CUDA_TRY(cudaGetLastError());
+    int hflag = 0;
+    QRB_CUDA_TRY(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    QRB_CUDA_TRY(cudaStreamSynchronize(st));
+    g_launches += 2;
+    if (hflag) {
+      set_last_error("factorize: input matrix has non-finite entries");
+      return QRB_ENONFINITE;
+    }
+  }
+  const bool timing = std::getenv("QRB_TIMING") != nullptr;
+  double panel_ms = 0.0, update_ms = 0.0;
+  cudaEvent_t ep0 = nullptr, ep1 = nullptr, ep2 = nullptr;
+  if (timing) {
+    cudaEventCreate(&ep0);
+    cudaEventCreate(&ep1);
+    cudaEventCreate(&ep2);
+  }
+  QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
+  MatView A{h->A, h->m, h->n, h->lda};
+  for (int k = 0; k < h->npanels; ++k) {
+    const int64_t j0 = int64_t(k) * h->nb;
+    const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
+    const int64_t mk = h->m - j0;
+    double* Tk = h->T + int64_t(k) * h->nb * h->nb;
+    if (timing) cudaEventRecord(ep0, st);
+    QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, h->nb, ws, st));
+    if (timing) cudaEventRecord(ep1, st);
+    if (j0 + pw < h->n) {
+      QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, h->nb, A.sub(j0, j0 + pw, mk, h->n - j0 - pw),
+                       ws, st));
+    }
+    if (timing) {
+      cudaEventRecord(ep2, st);
+      cudaEventSynchronize(ep2);
+      panel_ms += elapsed(ep0, ep1);
+      update_ms += elapsed(ep1, ep2);
+    }
+  }
+  QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
+  QRB_CUDA_TRY(cudaEventSynchronize(h->ev1));
+  QRB_CUDA_TRY(cudaGetLastError());
+  if (timing) {
+    cudaEventDestroy(ep0);
+    cudaEventDestroy(ep1);
+    cudaEventDestroy(ep2);
+  }
+  h->factored = true;
+  h->rinv_ready = false;
+  if (rep) {
+    const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
+    rep->total_ms = elapsed(h->ev0, h->ev1);
+    rep->panel_ms = panel_ms;
+    rep->update_ms = update_ms;
+    rep->flops = 2.0 * m * n * n - 2.0 * n * n * n / 3.0;
+    rep->kernel_launches = g_launches.load() - launches0;
+  }
+  return QRB_OK;
+}
+
+int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt) {
+  if (!h || (T && ldt < h->nb)) return QRB_EARG;
+  DeviceGuard g(h->device);
+  if (tau)
+    QRB_CUDA_TRY(cudaMemcpyAsync(tau, h->tau, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
+                                 h->stream));
+  if (T)
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(T, ldt * sizeof(double), h->T, h->nb * sizeof(double),
+                                   h->nb * sizeof(double), int64_t(h->npanels) * h->nb,
+                                   cudaMemcpyDeviceToHost, h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return QRB_OK;
+}
+
+int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t ldt) {
+  if (!h || !tau || !T || ldt < h->nb) return QRB_EARG;
+  DeviceGuard g(h->device);
+  QRB_CUDA_TRY(cudaMemcpyAsync(h->tau, tau, sizeof(double) * h->n, cudaMemcpyHostToDevice,
+                               h->stream));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(h->T, h->nb * sizeof(double), T, ldt * sizeof(double),
+                                 h->nb * sizeof(double), int64_t(h->npanels) * h->nb,
+                                 cudaMemcpyHostToDevice, h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->factored = true;
+  h->rinv_ready = false;
+  return QRB_OK;
+}
+
+int qrb_get_rdiag(qrb_handle* h, double* diag) {
+  if (!h || !diag) return QRB_EARG;
+  DeviceGuard g(h->device);
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(diag, sizeof(double), h->A, (h->lda + 1) * sizeof(double),
+                                 sizeof(double), h->n, cudaMemcpyDeviceToHost, h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return QRB_OK;
+}
+
+int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double* X, int64_t ldx,
+              double* resid, int on_device, int64_t report_block, qrb_report* rep) {
+  clear_report(rep);
+  if (!h || !B || !X || nrhs < 0 || ldb < h->m || ldx < h->n) {
+    set_last_error("qrb_solve: bad arguments");
+    return QRB_EARG;
+  }
+  if (!h->factored) {
+    set_last_error("qrb_solve: matrix not factorized");
+    return QRB_ESTATE;
+  }
+  DeviceGuard g(h->device);
+  if (nrhs == 0) return QRB_OK;
+  const int64_t launches0 = g_launches.load();
+  // singularity rule first (the reference raises before touching B's result)
+  std::vector<double> diag(h->n);
+  QRB_TRY(qrb_get_rdiag(h, diag.data()));
+  const int64_t bad = singular_column(diag, report_block);
+  if (bad >= 0) {
+    set_last_error("singular upper-triangular factor: zero pivot at global column " +
+                   std::to_string(bad));
+    return static_cast<int>(1 + bad);
+  }
+  Workspace& ws = device_workspace();
+  cudaStream_t st = h->stream;
+  const int64_t ldw = (h->m + 31) & ~int64_t(31);
+  QRB_TRY(h->Bw.ensure(sizeof(double) * ldw * nrhs, st));
+  double* Bw = h->Bw.d();
+  QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(Bw, ldw * sizeof(double), B, ldb * sizeof(double),
+                                 h->m * sizeof(double), nrhs,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
+  QRB_TRY(ensure_rinv(h));
+  MatView A{h->A, h->m, h->n, h->lda};
+  MatView Bv{Bw, h->m, nrhs, ldw};
+  for (int k = 0; k < h->npanels; ++k) {
+    const int64_t j0 = int64_t(k) * h->nb;
+    const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
+    const int64_t mk = h->m - j0;
+    QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), h->T + int64_t(k) * h->nb * h->nb, h->nb,
+                     Bv.sub(j0, 0, mk, nrhs), ws, st));
+  }
+  if (resid) {
+    QRB_TRY(h->resid.ensure(sizeof(double) * nrhs, st));
+    QRB_TRY(column_sumsq(Bw, ldw, static_cast<int>(h->n), static_cast<int>(h->m),
+                         static_cast<int>(nrhs), h->resid.d(), st));
+    g_launches += 1;
+  }
+  QRB_TRY(trsm_upper(A.sub(0, 0, h->n, h->n), h->Rinv, h->nb, Bv.sub(0, 0, h->n, nrhs), st));
+  QRB_CUDA_TRY(cudaEventRecord(h->ev2, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(X, ldx * sizeof(double), Bw, ldw * sizeof(double),
+                                 h->n * sizeof(double), nrhs,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  std::vector<double> rs;
+  if (resid) {
+    rs.resize(nrhs);
+    QRB_CUDA_TRY(cudaMemcpyAsync(rs.data(), h->resid.d(), sizeof(double) * nrhs,
+                                 cudaMemcpyDeviceToHost, st));
+  }
+  QRB_CUDA_TRY(cudaStreamSynchronize(st));
+  QRB_CUDA_TRY(cudaGetLastError());
+  if (resid) {
+    if (on_device) {
+      for (auto& v : rs) v = std::sqrt(v);
+      QRB_CUDA_TRY(cudaMemcpy(resid, rs.data(), sizeof(double) * nrhs, cudaMemcpyHostToDevice));
+    } else {
+      for (int64_t j = 0; j < nrhs; ++j) resid[j] = std::sqrt(rs[j]);
+    }
+  }
+  if (rep) {
+    cudaEvent_t e3;
+    cudaEventCreate(&e3);
+    cudaEventRecord(e3, st);
+    cudaEventSynchronize(e3);
+    rep->h2d_ms = on_device ? 0.0 : elapsed(h->ev0, h->ev1);
+    rep->update_ms = elapsed(h->ev1, h->ev2);
+    rep->d2h_ms = on_device ? 0.0 : elapsed(h->ev2, e3);
+    rep->total_ms = elapsed(h->ev0, e3);
+    cudaEventDestroy(e3);
+    const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
+    rep->flops = (4.0 * m * n - n * n) * static_cast<double>(nrhs);
+    rep->kernel_launches = g_launches.load() - launches0;
+    rep->h2d_bytes = on_device ? 0 : h->m * nrhs * 8;
+    rep->d2h_bytes = on_device ? 0 : h->n * nrhs * 8;
+  }
+  return QRB_OK;
+}
+
+int qrb_op_panel(double* panel, int64_t ldp, int64_t m, int64_t w, double* tau, double* T,
+                 int64_t ldt, void* stream) {
+  if (!panel || !tau || !T || w < 1 || w > 128 || m < w || (ldp & 1) || ldt < w) {
+    set_last_error("qrb_op_panel: bad arguments");
+    return QRB_EARG;
+  }
+  MatView pv{panel, m, w, ldp};
+  return factor_panel(pv, tau, T, ldt, device_workspace(), static_cast<cudaStream_t>(stream));
+}
+
+int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
+                    int64_t ldt, double* C, int64_t ldc, int64_t nc, void* stream) {
+  if (!V || !T || !C || w < 1 || m < w || (ldv & 1) || (ldc & 1) || (ldt & 1) || ldt < w) {
+    set_last_error("qrb_op_apply_qt: bad arguments (leading dimensions must be even)");
+    return QRB_EARG;
+  }
+  MatView Vv{const_cast<double*>(V), m, w, ldv};
+  MatView Cv{C, m, nc, ldc};
+  return apply_qt(Vv, T, ldt, Cv, device_workspace(), static_cast<cudaStream_t>(stream));
+}
+
+int qrb_op_gemm_nn_sub(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                       int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream) {
+  if (!A || !B || !C || m < 0 || n < 0 || k < 0 || (lda & 1) || (ldb & 1) || (ldc & 1)) {
+    set_last_error("qrb_op_gemm_nn_sub: bad arguments (leading dimensions must be even)");
+    return QRB_EARG;
+  }
+  if (m == 0 || n == 0 || k == 0) return QRB_OK;
+  MatView Av{const_cast<double*>(A), m, k, lda};
+  MatView Bv{const_cast<double*>(B), k, n, ldb};
+  g_launches += 1;
+  return gemm_nn(Av, Bv, C, ldc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                 GEMM_EPI_SUB, 0, static_cast<cudaStream_t>(stream));
+}
+
+int qrb_op_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                   int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int mask_a,
+                   int mask_b, void* stream) {
+  if (!A || !B || !C || m < 0 || n < 0 || k < 0 || splits < 1 || (lda & 1) || (ldb & 1)) {
+    set_last_error("qrb_op_gemm_tn: bad arguments (leading dimensions must be even)");
+    return QRB_EARG;
+  }
+  if (m == 0 || n == 0) return QRB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MatView Av{const_cast<double*>(A), k, m, lda};
+  MatView Bv{const_cast<double*>(B), k, n, ldb};
+  if (splits == 1) {
+    g_launches += 1;
+    return gemm_tn(Av, Bv, C, ldc, 0, static_cast<int>(m), static_cast<int>(n),
+                   static_cast<int>(k), 1, mask_a, mask_b, st);
+  }
+  Workspace& ws = device_workspace();
+  const int64_t per = ldc * n;
+  int used = 0;
+  QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+  QRB_TRY(gemm_tn_split(Av, Bv, ws.Wparts.d(), ldc, per, static_cast<int>(m), static_cast<int>(n),
+                        static_cast<int>(k), splits, mask_a, mask_b, st, &used));
+  QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, static_cast<int>(m), static_cast<int>(n), ldc, C,
+                        ldc, st));
+  g_launches += 2;
+  return QRB_OK;
+}
+
+int qrb_op_trsm_upper(const double* R, int64_t ldr, int64_t n, int nb, double* B, int64_t ldb,
+                      int64_t nrhs, void* stream) {
+  if (!R || !B || n < 0 || nrhs < 0 || nb < 16 || nb > 128 || (nb % 16) || (ldr & 1) ||
+      (ldb & 1)) {
+    set_last_error("qrb_op_trsm_upper: bad arguments");
+    return QRB_EARG;
+  }
+  if (n == 0 || nrhs == 0) return QRB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace& ws = device_workspace();
+  const int nblk = static_cast<int>((n + nb - 1) / nb);
+  QRB_TRY(ws.Wparts.ensure(sizeof(double) * nb * nb * nblk, st));
+  QRB_TRY(trtri_blocks(R, ldr, static_cast<int>(n), nb, ws.Wparts.d(), st));
+  g_launches += 1;
+  MatView Rv{const_cast<double*>(R), n, n, ldr};
+  MatView Bv{B, n, nrhs, ldb};
+  return trsm_upper(Rv, ws.Wparts.d(), nb, Bv, st);
+}
+
+int qrb_release_workspace(void) {
+  cudaDeviceSynchronize();
+  device_workspace().release();
+  return QRB_OK;
+}
+
+int64_t qrb_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

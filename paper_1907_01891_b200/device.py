@@ -1,0 +1,171 @@
+"""Python face of one GPU-resident QR factorization (wraps a ``qrb_handle``).
+
+``QrDevice`` holds the m x n matrix in HBM (column-major, leading dimension
+padded to 32), factors it in place with the sm_100a kernels and solves many
+right-hand sides against the stored factors.  Host arrays are numpy; device
+arrays are torch CUDA tensors holding a column-major matrix as a row-major
+tensor of shape ``(cols, ld)`` (see :func:`colmajor`).
+
+There is no CPU path: constructing a ``QrDevice`` without the native library
+raises :class:`~paper_1907_01891_b200.errors.NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .errors import SingularMatrixError
+
+
+def _host_f64_fortran(a: np.ndarray) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return np.asfortranarray(a)
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def colmajor(t) -> tuple[int, int, int, int]:
+    """(data_ptr, rows, cols, ld) of a torch tensor holding a column-major matrix.
+
+    A column-major ``rows x cols`` matrix with leading dimension ``ld`` is stored
+    as a contiguous torch tensor of shape ``(cols, ld)`` (rows = ld unless the
+    caller passes a narrower logical row count separately).
+    """
+    if t.dim() != 2 or not t.is_contiguous():
+        raise ValueError("expected a contiguous 2-D tensor of shape (cols, ld)")
+    cols, ld = t.shape
+    return t.data_ptr(), ld, cols, ld
+
+
+class QrDevice:
+    """One m x n fp64 matrix resident on one GPU, factored with panel width nb."""
+
+    def __init__(self, m: int, n: int, nb: int = 128, device: int = 0):
+        if m < n:
+            raise ValueError(f"matrix must have rows >= cols, got {m}x{n}")
+        self.lib = _native.load()
+        self.m, self.n, self.nb, self.device = int(m), int(n), int(nb), int(device)
+        h = ctypes.c_void_p()
+        _native.check(self.lib.qrb_create(self.device, self.m, self.n, self.nb, ctypes.byref(h)),
+                      "qrb_create")
+        self._h = h
+        self.npanels = -(-self.n // self.nb)
+        self.last_report: dict = {}
+
+    # -- lifecycle ----------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.qrb_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- matrix in / out -----------------------------------------------------
+    def set_matrix(self, a, col0: int = 0) -> None:
+        """Upload columns [col0, col0 + a.shape[1]) from a host array (m x k)."""
+        a = _host_f64_fortran(a)
+        if a.shape[0] != self.m:
+            raise ValueError(f"expected {self.m} rows, got {a.shape[0]}")
+        _native.check(self.lib.qrb_set_matrix(self._h, col0, a.shape[1], _ptr(a), self.m, 0),
+                      "qrb_set_matrix")
+
+    def set_matrix_device(self, t, col0: int = 0) -> None:
+        """Copy columns from a torch CUDA tensor of shape (k, ld) (column-major m x k)."""
+        ptr, _, cols, ld = colmajor(t)
+        _native.check(self.lib.qrb_set_matrix(self._h, col0, cols, ctypes.c_void_p(ptr), ld, 1),
+                      "qrb_set_matrix")
+
+    def get_matrix(self, col0: int = 0, ncols: int | None = None) -> np.ndarray:
+        """Factored storage (R on/above the diagonal, reflectors below), m x ncols."""
+        ncols = self.n - col0 if ncols is None else ncols
+        out = np.empty((self.m, ncols), dtype=np.float64, order="F")
+        _native.check(self.lib.qrb_get_matrix(self._h, col0, ncols, _ptr(out), self.m, 0),
+                      "qrb_get_matrix")
+        return out
+
+    def r_factor(self) -> np.ndarray:
+        return np.triu(self.get_matrix()[: self.n, :])
+
+    def rdiag(self) -> np.ndarray:
+        d = np.empty(self.n)
+        _native.check(self.lib.qrb_get_rdiag(self._h, _ptr(d)), "qrb_get_rdiag")
+        return d
+
+    def factors(self) -> tuple[np.ndarray, np.ndarray]:
+        """(tau[n], T stacked as nb x npanels*nb)."""
+        tau = np.empty(self.n)
+        t = np.empty((self.nb, self.npanels * self.nb), order="F")
+        _native.check(self.lib.qrb_get_factors(self._h, _ptr(tau), _ptr(t), self.nb),
+                      "qrb_get_factors")
+        return tau, t
+
+    def set_factors(self, tau: np.ndarray, t: np.ndarray) -> None:
+        tau = np.ascontiguousarray(tau, dtype=np.float64)
+        t = np.asfortranarray(t, dtype=np.float64)
+        if tau.shape != (self.n,) or t.shape != (self.nb, self.npanels * self.nb):
+            raise ValueError("factor shapes do not match this handle")
+        _native.check(self.lib.qrb_set_factors(self._h, _ptr(tau), _ptr(t), self.nb),
+                      "qrb_set_factors")
+
+    # -- compute --------------------------------------------------------------
+    def factorize(self) -> dict:
+        rep = _native.QrbReport()
+        _native.check(self.lib.qrb_factorize(self._h, ctypes.byref(rep)), "qrb_factorize")
+        self.last_report = rep.as_dict()
+        return self.last_report
+
+    def solve(self, b, report_block: int | None = None, want_resid: bool = True):
+        """X = R^-1 (Q^T B)[:n] for host B (m x nrhs); returns (X, resid, report)."""
+        b = _host_f64_fortran(b)
+        if b.shape[0] != self.m:
+            raise ValueError(f"right-hand side has {b.shape[0]} rows, expected {self.m}")
+        nrhs = b.shape[1]
+        x = np.empty((self.n, nrhs), order="F")
+        resid = np.empty(nrhs) if want_resid else None
+        rep = _native.QrbReport()
+        st = self.lib.qrb_solve(self._h, _ptr(b), self.m, nrhs, _ptr(x), self.n,
+                                _ptr(resid) if want_resid else None, 0,
+                                int(report_block or self.n), ctypes.byref(rep))
+        st = _native.check(st, "qrb_solve")
+        if st > 0:
+            raise SingularMatrixError(st - 1)
+        self.last_report = rep.as_dict()
+        return x, resid, self.last_report
+
+    def solve_device(self, b_t, x_t, resid_t=None, report_block: int | None = None) -> dict:
+        """Device-resident solve: b_t (nrhs, ldb) and x_t (nrhs, ldx) torch CUDA tensors."""
+        bp, _, nrhs, ldb = colmajor(b_t)
+        xp, _, nrhs2, ldx = colmajor(x_t)
+        if nrhs2 != nrhs or ldb < self.m or ldx < self.n:
+            raise ValueError("solve_device: shape mismatch")
+        rp = ctypes.c_void_p(resid_t.data_ptr()) if resid_t is not None else None
+        rep = _native.QrbReport()
+        st = self.lib.qrb_solve(self._h, ctypes.c_void_p(bp), ldb, nrhs, ctypes.c_void_p(xp), ldx,
+                                rp, 1, int(report_block or self.n), ctypes.byref(rep))
+        st = _native.check(st, "qrb_solve")
+        if st > 0:
+            raise SingularMatrixError(st - 1)
+        self.last_report = rep.as_dict()
+        return self.last_report
+
+
+def launch_count() -> int:
+    """Kernels launched by libqrb200 in this process so far."""
+    return int(_native.load().qrb_launch_count())
