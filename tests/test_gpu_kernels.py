@@ -1,0 +1,126 @@
+"""Kernel-level parity of the stream-ordered C-ABI operators (qrb_op_*)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from conftest import rel_err
+from oracle import tiled_qr as orc
+from paper_1907_01891_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def lib():
+    return _native.load()
+
+
+def to_dev(a, ld=None):
+    """numpy (rows x cols) -> torch (cols, ld) holding the column-major matrix."""
+    a = np.asarray(a, dtype=np.float64)
+    ld = ld or a.shape[0] + (a.shape[0] & 1)
+    t = torch.zeros((a.shape[1], ld), dtype=torch.float64, device="cuda")
+    t[:, :a.shape[0]] = torch.from_numpy(np.ascontiguousarray(a.T))
+    return t, ld
+
+
+def to_host(t, rows):
+    torch.cuda.synchronize()
+    return t[:, :rows].cpu().numpy().T.copy()
+
+
+def P(t, off=0):
+    return ctypes.c_void_p(t.data_ptr() + 8 * off)
+
+
+def unit_lower(v):
+    w = v.shape[1]
+    u = np.tril(v, -1)
+    u[np.arange(w), np.arange(w)] = 1.0
+    return u
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 16), (300, 70, 37), (1000, 513, 128), (64, 8, 3),
+                                   (4616, 5, 128), (130, 1, 1)])
+def test_gemm_nn_sub(m, n, k):
+    rng = np.random.default_rng(m + n + k)
+    A, B, C = (rng.standard_normal(s) for s in [(m, k), (k, n), (m, n)])
+    At, lda = to_dev(A)
+    Bt, ldb = to_dev(B)
+    Ct, ldc = to_dev(C)
+    assert lib().qrb_op_gemm_nn_sub(P(At), lda, P(Bt), ldb, P(Ct), ldc, m, n, k, None) == 0
+    assert rel_err(to_host(Ct, m), C - A @ B) <= 1e-13
+
+
+@pytest.mark.parametrize("k,m,n,splits", [(4616, 128, 5, 1), (4616, 128, 5, 18), (5000, 40, 70, 3),
+                                          (48, 128, 128, 4), (1000, 128, 1000, 2), (17, 3, 2, 1)])
+@pytest.mark.parametrize("mask_a,mask_b", [(0, 0), (1, 0), (1, 1)])
+def test_gemm_tn_with_unit_lower_masks(k, m, n, splits, mask_a, mask_b):
+    rng = np.random.default_rng(k + m + n)
+    A, B = rng.standard_normal((k, m)), rng.standard_normal((k, n))
+    Ae = unit_lower(A) if mask_a else A
+    Be = unit_lower(B) if mask_b else B
+    At, lda = to_dev(A)
+    Bt, ldb = to_dev(B)
+    Ct, ldc = to_dev(np.zeros((m, n)))
+    st = lib().qrb_op_gemm_tn(P(At), lda, P(Bt), ldb, P(Ct), ldc, m, n, k, splits, mask_a, mask_b,
+                              None)
+    assert st == 0
+    assert rel_err(to_host(Ct, m), Ae.T @ Be) <= 1e-13
+
+
+@pytest.mark.parametrize("m,w", [(64, 64), (500, 128), (2160, 128), (20000, 128), (70000, 128),
+                                 (3000, 56), (129, 1), (4000, 100)])
+def test_panel_matches_lapack_geqrf(m, w):
+    rng = np.random.default_rng(m + w)
+    a = rng.standard_normal((m, w))
+    t, ld = to_dev(a)
+    tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+    T = torch.zeros((w, 128), dtype=torch.float64, device="cuda")
+    assert lib().qrb_op_panel(P(t), ld, m, w, P(tau), P(T), 128, None) == 0
+    got = to_host(t, m)
+    (qr_raw, tau_ref), _ = sla.qr(a, mode="raw")
+    # same dlarfg sign convention: R, V and tau agree elementwise
+    assert rel_err(np.triu(got[:w]), np.triu(qr_raw[:w])) <= 1e-12
+    assert rel_err(np.tril(got, -1), np.tril(qr_raw, -1)) <= 1e-10
+    np.testing.assert_allclose(tau.cpu().numpy(), tau_ref, rtol=1e-12, atol=1e-14)
+    # T = the reference's forward T recurrence (kernels.py:134-147)
+    v = unit_lower(got)
+    taus = tau.cpu().numpy()
+    t_ref = orc._t_factor(lambda k: v[:, :k].T @ v[:, k], taus)
+    assert rel_err(T.cpu().numpy().T[:w, :w], t_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("m,w,nc", [(1000, 128, 77), (4616, 128, 5), (300, 32, 300)])
+def test_apply_qt_matches_oracle(m, w, nc):
+    rng = np.random.default_rng(m)
+    a = rng.standard_normal((m, w))
+    t, ld = to_dev(a)
+    tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+    T = torch.zeros((w, 128), dtype=torch.float64, device="cuda")
+    lib().qrb_op_panel(P(t), ld, m, w, P(tau), P(T), 128, None)
+    c = rng.standard_normal((m, nc))
+    ct, ldc = to_dev(c)
+    assert lib().qrb_op_apply_qt(P(t), ld, m, w, P(T), 128, P(ct), ldc, nc, None) == 0
+    got = to_host(ct, m)
+    v = unit_lower(to_host(t, m))
+    tf = T.cpu().numpy().T[:w, :w]
+    ref = c - v @ (tf.T @ (v.T @ c))
+    assert rel_err(got, ref) <= 1e-12
+    # Q^T preserves column norms
+    np.testing.assert_allclose(np.linalg.norm(got, axis=0), np.linalg.norm(c, axis=0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("n,nb,nrhs", [(300, 128, 5), (1000, 64, 33), (128, 128, 1), (77, 16, 8)])
+def test_trsm_upper(n, nb, nrhs):
+    rng = np.random.default_rng(n)
+    r = np.triu(rng.standard_normal((n, n))) + n * np.eye(n)
+    b = rng.standard_normal((n, nrhs))
+    rt, ldr = to_dev(r)
+    bt, ldb = to_dev(b)
+    assert lib().qrb_op_trsm_upper(P(rt), ldr, n, nb, P(bt), ldb, nrhs, None) == 0
+    assert rel_err(to_host(bt, n), sla.solve_triangular(r, b)) <= 1e-12

@@ -1,0 +1,219 @@
+"""Parity of the sm_100a path (through the C ABI) with the oracle and the
+reference's golden vectors.  Tolerances are BASELINE.json's: R up to per-row
+sign <= 1e-10 relative, x <= 1e-8 relative, residual within 1e-9 relative."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import rel_err, sign_normalise
+from oracle import tiled_qr as orc
+import paper_1907_01891_b200 as pkg
+from paper_1907_01891_b200 import ct_system as cs
+from paper_1907_01891_b200.device import QrDevice, launch_count
+
+pytestmark = pytest.mark.gpu
+
+R_TOL, X_TOL, RES_TOL = 1e-10, 1e-8, 1e-9
+
+
+def gpu_qr(a, nb=128):
+    q = QrDevice(a.shape[0], a.shape[1], nb)
+    q.set_matrix(a)
+    q.factorize()
+    return q
+
+
+# -- known answers -------------------------------------------------------------------
+
+
+def test_kat_two_vector_column_and_identity():
+    a = np.zeros((4, 4))
+    a[0, 0], a[1, 0] = 3.0, 4.0
+    with gpu_qr(a) as q:
+        assert abs(q.rdiag()[0]) == pytest.approx(5.0, rel=1e-15)
+    with gpu_qr(np.eye(8)) as q:
+        np.testing.assert_array_equal(q.get_matrix(), np.eye(8))
+        tau, _ = q.factors()
+        assert not tau.any()
+
+
+def test_kat_trsm_through_solve():
+    # A = [[2,1],[0,4]] (already upper triangular: no reflection), b = [5, 8]
+    with gpu_qr(np.array([[2.0, 1.0], [0.0, 4.0]])) as q:
+        x, res, _ = q.solve(np.array([[5.0], [8.0]]))
+    np.testing.assert_allclose(np.abs(x[:, 0]), [1.5, 2.0], rtol=1e-15)
+
+
+# -- reference shape grid -------------------------------------------------------------
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_grid_r_and_x_match_reference(golden, idx):
+    g = golden("ref_grid.npz")
+    with gpu_qr(g[f"g{idx}_a"]) as q:
+        assert rel_err(sign_normalise(q.r_factor()), g[f"g{idx}_r"]) <= R_TOL
+    with gpu_qr(g[f"g{idx}_aw"]) as q:
+        x, _, _ = q.solve(g[f"g{idx}_b"])
+    assert rel_err(x, g[f"g{idx}_x"]) <= X_TOL
+
+
+@pytest.mark.parametrize("nb", [16, 32, 64, 128])
+@pytest.mark.parametrize("shape", [(300, 200), (1000, 999), (777, 130), (2049, 257)])
+def test_ragged_shapes_against_oracle(shape, nb):
+    rng = np.random.default_rng(shape[0] + nb)
+    m, n = shape
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.linspace(100, 1, n)) @ v.T
+    x0 = rng.standard_normal((n, 7))
+    bm = a @ x0 + 1e-3 * rng.standard_normal((m, 7))
+    f = orc.factorize_dense(a, 256, 64)
+    x_ref = orc.solve_dense(f, bm)
+    with gpu_qr(a, nb) as q:
+        assert rel_err(sign_normalise(q.r_factor()), sign_normalise(f.r())) <= R_TOL
+        x, res, _ = q.solve(bm)
+    assert rel_err(x, x_ref) <= X_TOL
+    np.testing.assert_allclose(res, orc.residual_norms(f, bm), rtol=RES_TOL)
+
+
+# -- CT instances vs the reference run -------------------------------------------------
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_ct_instances_match_reference(golden, cfg):
+    ref = golden(f"ref_ct{cfg}.npz")
+    a = cs.dense_matrix(cs.config_geometry(cfg), order="C")
+    assert hashlib.sha256(a.tobytes()).hexdigest() == str(ref["a_sha256"])
+    with gpu_qr(a) as q:
+        r = sign_normalise(q.r_factor())
+        x, res, rep = q.solve(ref["b"])
+    if "r_signed" in ref:
+        assert rel_err(r, ref["r_signed"]) <= R_TOL
+    else:
+        assert rel_err(r[:32], ref["r_rows32"]) <= R_TOL
+    np.testing.assert_allclose(np.abs(np.diag(r)), ref["rdiag_abs"], rtol=R_TOL)
+    assert rel_err(x, ref["x"]) <= X_TOL
+    np.testing.assert_allclose(res, ref["resid"], rtol=RES_TOL)
+    assert rep["kernel_launches"] > 0
+
+
+# -- the drop-in tile-store API --------------------------------------------------------
+
+
+def make_store(arr, b, directory):
+    m = pkg.TiledMatrix.create(arr.shape[0], arr.shape[1], b, directory)
+    pkg.scatter_matrix(m, arr)
+    return m
+
+
+def blk_bytes(directory):
+    return {p.name: p.read_bytes() for p in sorted(directory.glob("*.blk"))}
+
+
+@pytest.mark.parametrize("m,n,b", [(8, 8, 4), (12, 8, 4), (10, 7, 4), (13, 5, 4), (16, 16, 8),
+                                   (9, 9, 3), (300, 200, 64)])
+def test_dropin_factorize_solve(tmp_path, m, n, b):
+    rng = np.random.default_rng(m * 100 + n * 10 + b)
+    arr = rng.standard_normal((m, n))
+    bmat = rng.standard_normal((m, 3))
+    cfg = pkg.EngineConfig(tile_size=b, inner_block=min(64, b))
+    a = make_store(arr, b, tmp_path / "a")
+    rhs = make_store(bmat, b, tmp_path / "b")
+    before_a, before_b = blk_bytes(tmp_path / "a"), blk_bytes(tmp_path / "b")
+    factors, rep = pkg.factorize(a, cfg, tmp_path / "f")
+    got_r = np.triu(pkg.gather_matrix(factors.factored)[:n, :n])
+    f = orc.factorize_dense(arr, b, min(64, b))
+    assert rel_err(sign_normalise(got_r), sign_normalise(f.r())) <= R_TOL
+    x, srep = pkg.solve(factors, rhs, cfg, tmp_path / "out")
+    assert rel_err(pkg.gather_matrix(x), orc.solve_dense(f, bmat)) <= X_TOL
+    assert blk_bytes(tmp_path / "a") == before_a and blk_bytes(tmp_path / "b") == before_b
+    assert not (tmp_path / "out" / "work").exists()
+    assert rep.compute_seconds > 0 and "task_count" in rep.to_text()
+    # factor once, solve later from disk in a fresh handle
+    loaded = pkg.QrFactors.load(tmp_path / "f")
+    loaded.check_complete()
+    x2, _ = pkg.solve(loaded, rhs, cfg, tmp_path / "out2")
+    np.testing.assert_array_equal(pkg.gather_matrix(x2), pkg.gather_matrix(x))
+
+
+@pytest.mark.parametrize("name", ["c6", "c3_19", "c0"])
+def test_singular_column_matches_reference(golden, tmp_path, name):
+    z = golden("ref_singular.npz")
+    b = int(z[f"{name}_tile"][0])
+    cfg = pkg.EngineConfig(tile_size=b, inner_block=min(64, b))
+    a = make_store(z[f"{name}_a"], b, tmp_path / "a")
+    rhs = make_store(z[f"{name}_b"], b, tmp_path / "b")
+    factors, _ = pkg.factorize(a, cfg, tmp_path / "f")
+    with pytest.raises(pkg.SingularMatrixError) as e:
+        pkg.solve(factors, rhs, cfg, tmp_path / "out")
+    assert e.value.global_column == int(z[f"{name}_col"][0])
+
+
+def test_nonfinite_rejected(tmp_path):
+    arr = np.eye(8)
+    arr[3, 2] = np.nan
+    a = make_store(arr, 4, tmp_path / "a")
+    with pytest.raises(pkg.KernelInputError):
+        pkg.factorize(a, pkg.EngineConfig(tile_size=4, inner_block=4), tmp_path / "f")
+
+
+def test_zero_rhs_gives_zero_and_identity_factors(tmp_path):
+    rng = np.random.default_rng(3)
+    a = make_store(rng.standard_normal((8, 8)), 4, tmp_path / "a")
+    rhs = make_store(np.zeros((8, 2)), 4, tmp_path / "b")
+    cfg = pkg.EngineConfig(tile_size=4, inner_block=4)
+    factors, _ = pkg.factorize(a, cfg, tmp_path / "f")
+    x, _ = pkg.solve(factors, rhs, cfg, tmp_path / "out")
+    np.testing.assert_array_equal(pkg.gather_matrix(x), np.zeros((8, 2)))
+    ident = make_store(np.eye(8), 4, tmp_path / "i")
+    fi, _ = pkg.factorize(ident, cfg, tmp_path / "fi")
+    np.testing.assert_array_equal(pkg.gather_matrix(fi.factored), np.eye(8))
+
+
+def test_truncated_factor_tile_raises_task_io_error(tmp_path):
+    rng = np.random.default_rng(19)
+    a = make_store(rng.standard_normal((8, 8)), 4, tmp_path / "a")
+    cfg = pkg.EngineConfig(tile_size=4, inner_block=4)
+    pkg.factorize(a, cfg, tmp_path / "f", keep_on_device=False)
+    loaded = pkg.QrFactors.load(tmp_path / "f")
+    p = loaded.factored.tile_path(pkg.TileId(0, 0))
+    p.write_bytes(p.read_bytes()[:10])
+    rhs = make_store(np.ones((8, 1)), 4, tmp_path / "b")
+    with pytest.raises(pkg.TaskIoError) as e:
+        pkg.solve(loaded, rhs, cfg, tmp_path / "out")
+    assert e.value.seq == 0
+
+
+def test_solve_rejects_mismatches(tmp_path):
+    a = make_store(np.eye(8), 8, tmp_path / "a")
+    factors, _ = pkg.factorize(a, pkg.EngineConfig(tile_size=8, inner_block=4), tmp_path / "f")
+    with pytest.raises(ValueError, match="inner_block"):
+        pkg.solve(factors, make_store(np.ones((8, 1)), 8, tmp_path / "b"),
+                  pkg.EngineConfig(tile_size=8, inner_block=8), tmp_path / "o")
+    with pytest.raises(ValueError, match="rows"):
+        pkg.solve(factors, make_store(np.ones((12, 1)), 8, tmp_path / "b2"),
+                  pkg.EngineConfig(tile_size=8, inner_block=4), tmp_path / "o2")
+
+
+# -- determinism and the native-path evidence --------------------------------------------
+
+
+def test_run_to_run_bitwise_determinism():
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((3000, 1100))
+    bm = rng.standard_normal((3000, 9))
+    outs = []
+    for _ in range(2):
+        with gpu_qr(a) as q:
+            x, res, _ = q.solve(bm)
+            outs.append((q.get_matrix().tobytes(), x.tobytes(), res.tobytes()))
+    assert outs[0] == outs[1]
+
+
+def test_kernels_actually_launch():
+    before = launch_count()
+    with gpu_qr(np.random.default_rng(0).standard_normal((512, 256))) as q:
+        q.solve(np.ones((512, 2)))
+    assert launch_count() > before + 10
