@@ -260,7 +260,7 @@ def _factor_dir_writes(factors: QrFactors, dev: QrDevice, directory: Path) -> tu
         written += factors.factored.write_column_block(j, blk)
     tau, t = dev.factors()
     tau.astype("<f8").tofile(directory / _TAU_NAME)
-    np.asfortranarray(t).astype("<f8").tofile(directory / _T_NAME)
+    t.astype("<f8").ravel(order="F").tofile(directory / _T_NAME)
     return time.perf_counter() - t0, written
 
 

@@ -38,9 +38,9 @@ def P(t, off=0):
 
 
 def unit_lower(v):
-    w = v.shape[1]
+    d = min(v.shape)
     u = np.tril(v, -1)
-    u[np.arange(w), np.arange(w)] = 1.0
+    u[np.arange(d), np.arange(d)] = 1.0
     return u
 
 

@@ -75,7 +75,10 @@ def test_ragged_shapes_against_oracle(shape, nb):
         assert rel_err(sign_normalise(q.r_factor()), sign_normalise(f.r())) <= R_TOL
         x, res, _ = q.solve(bm)
     assert rel_err(x, x_ref) <= X_TOL
-    np.testing.assert_allclose(res, orc.residual_norms(f, bm), rtol=RES_TOL)
+    # residual within 1e-9 relative; a near-zero residual (m - n tiny) is only
+    # defined to rounding of ||b||, so the absolute floor is 1e-12 ||b_j||
+    np.testing.assert_allclose(res, orc.residual_norms(f, bm), rtol=RES_TOL,
+                               atol=1e-12 * np.linalg.norm(bm, axis=0).max())
 
 
 # -- CT instances vs the reference run -------------------------------------------------
