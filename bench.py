@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: fp64 blocked Householder QR of the CT system
+matrix + multi-slice solve, on BASELINE.json's configuration 3 (256x256 image,
+180 views x 384 bins -> A = 69120 x 65536 fp64, 36 GB; 256 noisy sinograms).
+
+One step = reset A in HBM from its pristine copy (device-to-device), factor it
+(qrb_factorize) and solve the slice batch against the new factors
+(qrb_solve, device-resident B / X).  ``value`` is the QR TFLOP/s over the timed
+steps (algorithmic 2mn^2 - 2n^3/3 flops / device time of the factorizations);
+slices/s of the solve is reported beside it.  ``e2e`` repeats a step through
+the public host-buffer API: pinned-host A and B copied in, X and the residual
+norms copied out, all inside the timed region.
+
+``--impl reference`` times the reference algorithm (the oracle restatement of
+oocqr's tiled QR, run on the host cores) on a bounded sample of the same
+workload: the leading 69120 x 1024 column block of the same matrix.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+For N > 1 launch under torchrun (one rank per GPU).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fp64 QR TFLOP/s (% of FP64 peak) at 1/2/4/8 GPUs; solved slices/sec"
+UNIT = "TFLOP/s"
+# measured FP64 tensor (DMMA.8x8x4) issue-rate peak of this pool's B200 at
+# 1965 MHz, profiles/r01_fp64_pipe_probe.log (MEASURED_PEAKS.json has no fp64 entry)
+FP64_PEAK_TFLOPS = 37.09
+FP64_PEAK_SOURCE = "measured DMMA peak, profiles/r01_fp64_pipe_probe.log"
+CPU_SAMPLE_COLS = 1024
+
+
+def qr_flops(m: int, n: int) -> float:
+    return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
+
+
+def solve_flops(m: int, n: int, s: int) -> float:
+    return (4.0 * m * n - n * n) * s
+
+
+# -- clocks sampler ---------------------------------------------------------------------
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int = 0):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -- workload ------------------------------------------------------------------------------
+
+
+def build_workload(cfg: int, slices: int | None):
+    from paper_1907_01891_b200 import ct_system as cs
+    g = cs.config_geometry(cfg)
+    s = slices or cs.CONFIGS[cfg]["slices"]
+    coo = cs.siddon_coo(g)
+    x_true = cs.phantom_stack(cfg, s)
+    return g, coo, x_true, s
+
+
+def densify_device(g, coo, lda: int):
+    """Dense column-major A on the GPU (torch tensor (n, lda)) from host COO."""
+    import torch
+    r, c, v = coo
+    a = torch.zeros((g.n_pixels, lda), dtype=torch.float64, device="cuda")
+    flat = torch.from_numpy(c * lda + r).cuda()
+    a.view(-1).index_put_((flat,), torch.from_numpy(v).cuda())
+    return a
+
+
+def cpu_sample_tflops(coo, g, steps: int = 1):
+    """Reference algorithm (oracle port, tiled left-looking QR of oocqr) on the
+    leading m x 1024 column block of A; returns (TFLOP/s, seconds per run)."""
+    from oracle.tiled_qr import factorize_dense
+    r, c, v = coo
+    ncol = min(CPU_SAMPLE_COLS, g.n_pixels)
+    sel = c < ncol
+    a = np.zeros((g.n_rays, ncol))
+    a[r[sel], c[sel]] = v[sel]
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        factorize_dense(a, 1024, 128)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    return qr_flops(g.n_rays, ncol) / t / 1e12, t, ncol
+
+
+def reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    g, coo, _, _ = build_workload(args.config, 1)
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_sample_tflops(coo, g)
+    val, t, ncol = cpu_sample_tflops(coo, g, steps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Siddon fan-beam A, seeded)",
+        "config": {"workload": f"config{args.config}: QR sample = leading {g.n_rays}x{ncol} "
+                               f"column block of A", "m": g.n_rays, "n": ncol,
+                   "tile_size": 1024, "inner_block": 128},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
+                                   f"({g.n_rays}x{ncol}), b=1024, w=128"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -- our arm -----------------------------------------------------------------------------------
+
+
+def ours_arm(args, rank: int, world: int):
+    import torch
+    from paper_1907_01891_b200 import ct_system as cs
+    from paper_1907_01891_b200.device import QrDevice, launch_count
+
+    if world > 1:
+        from paper_1907_01891_b200 import dist
+        return dist.bench_rank(args, rank, world)
+
+    torch.cuda.set_device(0)
+    t_setup = time.perf_counter()
+    g, coo, x_true, S = build_workload(args.config, args.slices)
+    m, n = g.n_rays, g.n_pixels
+    lda = (m + 31) // 32 * 32
+    a_dev = densify_device(g, coo, lda)
+    # sinograms b = A x + 1% noise (seeded per slice); A x via the device matrix
+    xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()        # (S, n)
+    ax = (xt @ a_dev[:, :m]).cpu().numpy().T                            # (m, S)
+    b_host = cs.noisy_sinograms(ax, args.config)
+    ldb = lda
+    b_dev = torch.zeros((S, ldb), dtype=torch.float64, device="cuda")
+    b_dev[:, :m] = torch.from_numpy(np.ascontiguousarray(b_host.T)).cuda()
+    x_dev = torch.zeros((S, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+    r_dev = torch.zeros(S, dtype=torch.float64, device="cuda")
+    del xt
+    q = QrDevice(m, n, args.nb)
+    q.set_profiling(True)
+    setup_s = time.perf_counter() - t_setup
+
+    def step():
+        q.set_matrix_device(a_dev)
+        frep = q.factorize()
+        srep = q.solve_device(b_dev, x_dev, r_dev)
+        return frep, srep
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    sampler.start()
+    launches0 = launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    freps, sreps = [], []
+    for _ in range(args.steps):
+        fr, sr = step()
+        freps.append(fr)
+        sreps.append(sr)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = launch_count() - launches0
+    step_ms = e0.elapsed_time(e1) / args.steps
+    f_ms = float(np.mean([r["total_ms"] for r in freps]))
+    s_ms = float(np.mean([r["total_ms"] for r in sreps]))
+    fl = qr_flops(m, n)
+    value = fl / (f_ms * 1e-3) / 1e12
+    slices_per_s = S / (s_ms * 1e-3)
+
+    # dominant kernel roofline from the live CUDA-event kernel accounting
+    kstats: dict = {}
+    for rep in freps + sreps:
+        for name, k in rep["kernels"].items():
+            acc = kstats.setdefault(name, {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
+            for key in acc:
+                acc[key] += k[key]
+    dom = max((k for k in kstats if k.startswith("gemm")), key=lambda k: kstats[k]["ms"])
+    dk = kstats[dom]
+    achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": UNIT,
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "kernel": dom,
+                "peak_source": FP64_PEAK_SOURCE,
+                "per_launch_flops": dk["flops"] / dk["launches"],
+                "avg_launch_ms": dk["ms"] / dk["launches"]}
+    shares = {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4) for k, v in kstats.items()}
+
+    # residual sanity of the last step: GPU residual identity vs explicit ||Ax - b||
+    x_last = x_dev[:, :n]
+    r_explicit = torch.linalg.norm(x_last @ a_dev[:, :m] - b_dev[:, :m], dim=1)
+    resid_rel = float((torch.abs(r_explicit - r_dev) / r_explicit).max())
+
+    # end-to-end through the public host API (pinned host A and B, host X out)
+    a_pin = torch.empty((n, lda), dtype=torch.float64, pin_memory=True)
+    a_pin.copy_(a_dev)
+    b_pin = torch.empty((S, ldb), dtype=torch.float64, pin_memory=True)
+    b_pin.copy_(b_dev)
+    x_pin = torch.empty((S, n), dtype=torch.float64, pin_memory=True)
+    a_view = a_pin.numpy().T[:m, :]          # m x n column-major view, ld = lda
+    b_view = b_pin.numpy().T[:m, :]
+    x_view = x_pin.numpy().T                 # n x S column-major
+    del a_dev
+    torch.cuda.empty_cache()
+    q.set_profiling(False)
+    e2e_steps = max(1, args.e2e_steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(e2e_steps):
+        q.set_matrix(a_view)
+        q.factorize()
+        _, resid_host, _ = q.solve(b_view, out=x_view)
+    e3.record()
+    torch.cuda.synchronize()
+    e2e_s = max(e2.elapsed_time(e3) * 1e-3, 0.0) / e2e_steps
+    wall_e2e = (time.perf_counter() - t0) / e2e_steps
+    e2e = {"value": fl / e2e_s / 1e12, "unit": UNIT,
+           "h2d_bytes_per_step": int(m * n * 8 + m * S * 8),
+           "d2h_bytes_per_step": int(n * S * 8 + S * 8),
+           "ms_per_step": e2e_s * 1e3, "wall_ms_per_step": wall_e2e * 1e3,
+           "slices_per_s": S / e2e_s,
+           "path": "QrDevice.set_matrix(pinned host) + factorize + solve(host B -> host X)"}
+    q.close()
+
+    cores = len(os.sched_getaffinity(0))
+    cpu_val, cpu_t, ncol = cpu_sample_tflops(coo, g)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Siddon fan-beam A from seeded geometry; seeded 10-ellipse phantoms, "
+                "1% Gaussian noise)",
+        "config": {"workload": f"config{args.config}: QR of A {m}x{n} fp64 + solve {S} slices",
+                   "m": m, "n": n, "slices": S, "panel_width": args.nb,
+                   "parallelism": "single GPU",
+                   "l2": "inputs (A = %.1f GB) larger than L2 (126 MB)" % (m * n * 8 / 1e9)},
+        "pct_fp64_peak": value / FP64_PEAK_TFLOPS,
+        "slices_per_s": slices_per_s,
+        "solve_tflops": solve_flops(m, n, S) / (s_ms * 1e-3) / 1e12,
+        "factor_ms": f_ms, "solve_ms": s_ms,
+        "roofline": roofline, "kernel_time_share": shares,
+        "cpu_baseline": {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
+                                   f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "check": {"resid_identity_max_rel": resid_rel},
+        "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--slices", type=int, default=None)
+    ap.add_argument("--nb", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    ours_arm(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

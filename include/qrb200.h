@@ -55,6 +55,23 @@ typedef struct qrb_handle qrb_handle;
 
 /* Timing/accounting of one call; mirrors the reference RunReport
  * (task_engine.py:136-181) with device-side (CUDA event) times. */
+/* Per-kernel-family accounting, filled when profiling is on (qrb_set_profiling):
+ * device time from CUDA events on the launching stream around each launch,
+ * algorithmic flops / bytes of those launches. */
+typedef struct qrb_kernel_stat {
+  double ms;
+  double flops;
+  double bytes;
+  int64_t launches;
+} qrb_kernel_stat;
+
+#define QRB_K_PANEL 0   /* panel geqr2 + larft (incl. its inner block updates) */
+#define QRB_K_GEMM_TN 1 /* W = V^T C (DMMA, split-K + reduce)                  */
+#define QRB_K_GEMM_TT 2 /* W2 = T^T W                                          */
+#define QRB_K_GEMM_NN 3 /* C -= V W2 (DMMA)                                    */
+#define QRB_K_TRSM 4    /* back substitution                                    */
+#define QRB_K_COUNT 8
+
 typedef struct qrb_report {
   double total_ms;     /* whole call, CUDA events on the handle stream        */
   double panel_ms;     /* panel factorization (geqr2 + larft) share           */
@@ -66,6 +83,7 @@ typedef struct qrb_report {
   int64_t kernel_launches; /* kernels this library launched for the call     */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  qrb_kernel_stat kernels[QRB_K_COUNT];
 } qrb_report;
 
 /* library */
@@ -91,6 +109,9 @@ QRB_API int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const dou
                    int src_on_device);
 QRB_API int qrb_get_matrix(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
                    int dst_on_device);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event accounting in qrb_report.kernels. */
+QRB_API int qrb_set_profiling(qrb_handle* h, int on);
 
 /* In-place blocked Householder QR of the handle's matrix.
  * Replaces: factorize -> execute(gen_factorization_tasks) (task_engine.py:606-641,

@@ -29,6 +29,14 @@ QRB_ESTATE = -5
 QRB_EUNSUPPORTED = -6
 
 
+KERNEL_NAMES = ("panel", "gemm_tn", "gemm_tt", "gemm_nn", "trsm", "k5", "k6", "k7")
+
+
+class QrbKernelStat(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double), ("flops", ctypes.c_double),
+                ("bytes", ctypes.c_double), ("launches", c_i64)]
+
+
 class QrbReport(ctypes.Structure):
     """Mirror of ``qrb_report`` (include/qrb200.h)."""
 
@@ -43,10 +51,15 @@ class QrbReport(ctypes.Structure):
         ("kernel_launches", c_i64),
         ("h2d_bytes", c_i64),
         ("d2h_bytes", c_i64),
+        ("kernels", QrbKernelStat * 8),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        d = {name: getattr(self, name) for name, _ in self._fields_ if name != "kernels"}
+        d["kernels"] = {KERNEL_NAMES[i]: {"ms": k.ms, "flops": k.flops, "bytes": k.bytes,
+                                          "launches": int(k.launches)}
+                        for i, k in enumerate(self.kernels) if k.launches}
+        return d
 
 
 # exported symbol -> (restype, argtypes); the list IS the C ABI of include/qrb200.h
@@ -59,6 +72,7 @@ SIGNATURES = {
     "qrb_destroy": (c_int, [c_void_p]),
     "qrb_set_matrix": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_int]),
     "qrb_get_matrix": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_int]),
+    "qrb_set_profiling": (c_int, [c_void_p, c_int]),
     "qrb_factorize": (c_int, [c_void_p, ctypes.POINTER(QrbReport)]),
     "qrb_get_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_set_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),

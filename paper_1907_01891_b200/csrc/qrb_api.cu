@@ -75,6 +75,65 @@ struct Workspace {
 
 static std::atomic<int64_t> g_launches{0};
 
+// ---------------------------------------------------------------------------
+// optional per-kernel-family CUDA-event accounting (qrb_set_profiling)
+// ---------------------------------------------------------------------------
+struct Profiler {
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<Rec> recs;
+  int depth = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void reset() {
+    used = 0;
+    recs.clear();
+    depth = 0;
+  }
+  ~Profiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+static thread_local Profiler* g_prof = nullptr;
+
+struct ProfScope {
+  Profiler* p;
+  cudaStream_t st;
+  Profiler::Rec rec;
+  bool active;
+  ProfScope(int kind, double flops, double bytes, cudaStream_t s)
+      : p(g_prof), st(s), active(false) {
+    if (p && p->depth == 0) {
+      rec.kind = kind;
+      rec.flops = flops;
+      rec.bytes = bytes;
+      rec.a = p->get();
+      rec.b = p->get();
+      cudaEventRecord(rec.a, st);
+      active = true;
+    }
+    if (p) p->depth++;
+  }
+  ~ProfScope() {
+    if (p) p->depth--;
+    if (active) {
+      cudaEventRecord(rec.b, st);
+      p->recs.push_back(rec);
+    }
+  }
+};
+
 static Workspace& device_workspace() {
   static Workspace ws[64];
   int dev = 0;
@@ -97,30 +156,52 @@ static int apply_qt(const MatView& V, const double* T, int64_t ldt, const MatVie
   const int64_t per_split = ldw * nc;
   const int max_splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(32) << 20) / per_split)));
   const int splits = gemm_pick_splits(w, nc, m, max_splits);
-  if (splits > 1) {
-    QRB_TRY(ws.Wparts.ensure(sizeof(double) * per_split * splits, st));
-    int used = 0;
-    QRB_TRY(gemm_tn_split(V, C, ws.Wparts.d(), ldw, per_split, w, nc, m, splits, 1, 0, st, &used));
-    QRB_TRY(reduce_splits(ws.Wparts.d(), per_split, used, w, nc, ldw, ws.W.d(), ldw, st));
-    g_launches += 2;
-  } else {
-    QRB_TRY(gemm_tn(V, C, ws.W.d(), ldw, 0, w, nc, m, 1, 1, 0, st));
-    g_launches += 1;
+  const double fl = 2.0 * m * static_cast<double>(nc) * w;
+  {
+    ProfScope ps(QRB_K_GEMM_TN, fl, 8.0 * ((double)m * w + (double)m * nc + (double)w * nc), st);
+    if (splits > 1) {
+      QRB_TRY(ws.Wparts.ensure(sizeof(double) * per_split * splits, st));
+      int used = 0;
+      QRB_TRY(gemm_tn_split(V, C, ws.Wparts.d(), ldw, per_split, w, nc, m, splits, 1, 0, st,
+                            &used));
+      QRB_TRY(reduce_splits(ws.Wparts.d(), per_split, used, w, nc, ldw, ws.W.d(), ldw, st));
+      g_launches += 2;
+    } else {
+      QRB_TRY(gemm_tn(V, C, ws.W.d(), ldw, 0, w, nc, m, 1, 1, 0, st));
+      g_launches += 1;
+    }
   }
   // W2 = T^T W
   MatView Tv{const_cast<double*>(T), w, w, ldt};
   MatView Wv{ws.W.d(), w, nc, ldw};
-  QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
+  {
+    ProfScope ps(QRB_K_GEMM_TT, 2.0 * w * static_cast<double>(w) * nc,
+                 8.0 * (2.0 * w * nc + (double)w * w), st);
+    QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
+  }
   // C -= V W2
   MatView W2v{ws.W2.d(), w, nc, ldw};
-  QRB_TRY(gemm_nn(V, W2v, C.ptr, C.ld, m, nc, w, GEMM_EPI_SUB, 1, st));
+  {
+    ProfScope ps(QRB_K_GEMM_NN, fl, 8.0 * (2.0 * m * nc + (double)m * w + (double)w * nc), st);
+    QRB_TRY(gemm_nn(V, W2v, C.ptr, C.ld, m, nc, w, GEMM_EPI_SUB, 1, st));
+  }
   g_launches += 2;
   return QRB_OK;
 }
 
 // Householder QR of an m x w panel (w <= 128) in place, tau[w], T (w x w, ldt)
+static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64_t ldt,
+                             Workspace& ws, cudaStream_t st);
+
 static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
                         cudaStream_t st) {
+  const double m = static_cast<double>(panel.rows), w = static_cast<double>(panel.cols);
+  ProfScope ps(QRB_K_PANEL, 2.0 * m * w * w - 2.0 * w * w * w / 3.0, 16.0 * m * w, st);
+  return factor_panel_impl(panel, tau, T, ldt, ws, st);
+}
+
+static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64_t ldt,
+                             Workspace& ws, cudaStream_t st) {
   const int m = static_cast<int>(panel.rows);
   const int pw = static_cast<int>(panel.cols);
   if (pw <= 0) return QRB_OK;
@@ -180,6 +261,8 @@ static int trsm_upper(const MatView& R, const double* Rinv, int nb, const MatVie
   const int n = static_cast<int>(R.rows);
   const int nrhs = static_cast<int>(B.cols);
   if (n <= 0 || nrhs <= 0) return QRB_OK;
+  ProfScope ps(QRB_K_TRSM, static_cast<double>(n) * n * nrhs,
+               8.0 * (0.5 * n * (double)n + 2.0 * n * (double)nrhs), st);
   const int nblk = (n + nb - 1) / nb;
   for (int k = nblk - 1; k >= 0; --k) {
     const int i0 = k * nb;
@@ -244,6 +327,8 @@ struct qrb_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   DevBuf Bw;  // solve work buffer
   DevBuf resid;
+  bool profiling = false;
+  Profiler prof;
 };
 
 namespace {
@@ -270,6 +355,34 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
   cudaEventElapsedTime(&ms, a, b);
   return ms;
 }
+
+// activate the handle's profiler for one call; fold its records into rep at the end
+struct ProfSession {
+  qrb_handle* h;
+  explicit ProfSession(qrb_handle* hh) : h(hh) {
+    if (h->profiling) {
+      h->prof.reset();
+      g_prof = &h->prof;
+    }
+  }
+  void finish(qrb_report* rep) {
+    if (!h->profiling) return;
+    g_prof = nullptr;
+    if (!rep) return;
+    for (auto& r : h->prof.recs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      qrb_kernel_stat& k = rep->kernels[r.kind];
+      k.ms += ms;
+      k.flops += r.flops;
+      k.bytes += r.bytes;
+      k.launches += 1;
+    }
+  }
+  ~ProfSession() {
+    if (g_prof == &h->prof) g_prof = nullptr;
+  }
+};
 
 int ensure_rinv(qrb_handle* h) {
   if (h->rinv_ready) return QRB_OK;
@@ -357,6 +470,12 @@ int qrb_destroy(qrb_handle* h) {
   return QRB_OK;
 }
 
+int qrb_set_profiling(qrb_handle* h, int on) {
+  if (!h) return QRB_EARG;
+  h->profiling = on != 0;
+  return QRB_OK;
+}
+
 int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src, int64_t ld,
                    int src_on_device) {
   if (!h || !src || col0 < 0 || ncols < 0 || col0 + ncols > h->n || ld < h->m) {
@@ -416,6 +535,7 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   }
   const bool timing = std::getenv("QRB_TIMING") != nullptr;
   double panel_ms = 0.0, update_ms = 0.0;
+  ProfSession session(h);
   cudaEvent_t ep0 = nullptr, ep1 = nullptr, ep2 = nullptr;
   if (timing) {
     cudaEventCreate(&ep0);
@@ -453,6 +573,7 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   }
   h->factored = true;
   h->rinv_ready = false;
+  session.finish(rep);
   if (rep) {
     const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
     rep->total_ms = elapsed(h->ev0, h->ev1);
@@ -526,6 +647,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
   }
   Workspace& ws = device_workspace();
   cudaStream_t st = h->stream;
+  ProfSession session(h);
   const int64_t ldw = (h->m + 31) & ~int64_t(31);
   QRB_TRY(h->Bw.ensure(sizeof(double) * ldw * nrhs, st));
   double* Bw = h->Bw.d();
@@ -563,6 +685,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
   }
   QRB_CUDA_TRY(cudaStreamSynchronize(st));
   QRB_CUDA_TRY(cudaGetLastError());
+  session.finish(rep);
   if (resid) {
     if (on_device) {
       for (auto& v : rs) v = std::sqrt(v);

@@ -27,6 +27,19 @@ def _host_f64_fortran(a: np.ndarray) -> np.ndarray:
     return np.asfortranarray(a)
 
 
+def _host_colmajor(a: np.ndarray) -> tuple[np.ndarray, int]:
+    """(array, leading dimension) without copying when `a` is column-contiguous
+    with a padded leading dimension (e.g. a row slice of a pinned buffer)."""
+    a = np.asarray(a)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    if (a.dtype == np.float64 and a.strides[0] == 8 and a.strides[1] % 8 == 0
+            and a.strides[1] // 8 >= a.shape[0]):
+        return a, a.strides[1] // 8
+    a = np.asfortranarray(a, dtype=np.float64)
+    return a, a.shape[0]
+
+
 def _ptr(a: np.ndarray) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data)
 
@@ -79,12 +92,17 @@ class QrDevice:
 
     # -- matrix in / out -----------------------------------------------------
     def set_matrix(self, a, col0: int = 0) -> None:
-        """Upload columns [col0, col0 + a.shape[1]) from a host array (m x k)."""
-        a = _host_f64_fortran(a)
+        """Upload columns [col0, col0 + a.shape[1]) from a host array (m x k).
+        Column-contiguous arrays with a padded leading dimension (e.g. a view
+        of a pinned buffer) are copied without staging."""
+        a, ld = _host_colmajor(a)
         if a.shape[0] != self.m:
             raise ValueError(f"expected {self.m} rows, got {a.shape[0]}")
-        _native.check(self.lib.qrb_set_matrix(self._h, col0, a.shape[1], _ptr(a), self.m, 0),
+        _native.check(self.lib.qrb_set_matrix(self._h, col0, a.shape[1], _ptr(a), ld, 0),
                       "qrb_set_matrix")
+
+    def set_profiling(self, on: bool = True) -> None:
+        _native.check(self.lib.qrb_set_profiling(self._h, int(bool(on))), "qrb_set_profiling")
 
     def set_matrix_device(self, t, col0: int = 0) -> None:
         """Copy columns from a torch CUDA tensor of shape (k, ld) (column-major m x k)."""
@@ -131,16 +149,23 @@ class QrDevice:
         self.last_report = rep.as_dict()
         return self.last_report
 
-    def solve(self, b, report_block: int | None = None, want_resid: bool = True):
-        """X = R^-1 (Q^T B)[:n] for host B (m x nrhs); returns (X, resid, report)."""
-        b = _host_f64_fortran(b)
+    def solve(self, b, report_block: int | None = None, want_resid: bool = True, out=None):
+        """X = R^-1 (Q^T B)[:n] for host B (m x nrhs); returns (X, resid, report).
+        ``out`` may be a preallocated (n x nrhs) column-contiguous host array."""
+        b, ldb = _host_colmajor(b)
         if b.shape[0] != self.m:
             raise ValueError(f"right-hand side has {b.shape[0]} rows, expected {self.m}")
         nrhs = b.shape[1]
-        x = np.empty((self.n, nrhs), order="F")
+        if out is None:
+            x = np.empty((self.n, nrhs), order="F")
+            ldx = self.n
+        else:
+            x, ldx = _host_colmajor(out)
+            if x is not out or x.shape != (self.n, nrhs):
+                raise ValueError("out must be a column-contiguous (n x nrhs) float64 array")
         resid = np.empty(nrhs) if want_resid else None
         rep = _native.QrbReport()
-        st = self.lib.qrb_solve(self._h, _ptr(b), self.m, nrhs, _ptr(x), self.n,
+        st = self.lib.qrb_solve(self._h, _ptr(b), ldb, nrhs, _ptr(x), ldx,
                                 _ptr(resid) if want_resid else None, 0,
                                 int(report_block or self.n), ctypes.byref(rep))
         st = _native.check(st, "qrb_solve")
