@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace qrb {
@@ -275,6 +276,164 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// persistent C -= A B with TMA-staged C tiles (the trailing-update GEMM)
+//
+// One CTA per SM walks its share of the 128 x 64 output tiles.  The producer
+// warp streams A/B K-slices through the same 4-stage ring as above and, ahead
+// of every tile, TMA-loads the C tile into one of two 64 KB shared buffers.
+// The consumer warps subtract their register accumulators from the staged C
+// tile in shared memory and one thread TMA-stores it back, so the read-modify-
+// write of C (the HBM-bound part of a K = 128 update) overlaps the next tile's
+// DMMA main loop instead of stalling it.
+// ---------------------------------------------------------------------------
+constexpr int NN_BN = 64;
+constexpr uint32_t NN_A_BYTES = BM * BK * 8;
+constexpr uint32_t NN_B_BYTES = NN_BN * BK * 8;
+constexpr uint32_t NN_STAGE_BYTES = NN_A_BYTES + NN_B_BYTES;
+constexpr uint32_t NN_C_BYTES = BM * NN_BN * 8;
+constexpr int NN_SMEM = STAGES * NN_STAGE_BYTES + 2 * NN_C_BYTES + 1024 + 256;
+
+struct NnArgs {
+  int M, N, K;
+  int mask_a;
+  int group_m;
+  int num_tiles;
+};
+
+__device__ __forceinline__ void decode_tile(int tile, int num_m, int num_n, int group_m,
+                                            int& m_tile, int& n_tile) {
+  const int per_group = group_m * num_n;
+  const int first_m = (tile / per_group) * group_m;
+  const int gsize = min(num_m - first_m, group_m);
+  const int local = tile % per_group;
+  m_tile = first_m + local % gsize;
+  n_tile = local / gsize;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_nn_sub_persistent(const __grid_constant__ CUtensorMap mapA,
+                           const __grid_constant__ CUtensorMap mapB,
+                           const __grid_constant__ CUtensorMap mapC, const NnArgs args) {
+  constexpr int NT = NN_BN / 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* cbuf0 = smem + STAGES * NN_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf0 + 2 * NN_C_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* cfull = empty + STAGES;
+  uint64_t* cempty = cfull + 2;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + NN_BN - 1) / NN_BN;
+  const int num_k = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&cfull[b], 1);
+      mbar_init(&cempty[b], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {
+    if (lane == 0) {
+      prefetch_tmap(&mapA);
+      prefetch_tmap(&mapB);
+      prefetch_tmap(&mapC);
+      int kit = 0, it = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+        int m_tile, n_tile;
+        decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+        const int cb = it & 1;
+        if (it >= 2) mbar_wait(&cempty[cb], ((it >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&cfull[cb], NN_C_BYTES);
+        tma_load_2d(cbuf0 + cb * NN_C_BYTES, &mapC, m_tile * BM, n_tile * NN_BN, &cfull[cb]);
+        for (int kt = 0; kt < num_k; ++kt, ++kit) {
+          const int s = kit % STAGES;
+          if (kit >= STAGES) mbar_wait(&empty[s], ((kit / STAGES) & 1) ^ 1);
+          uint8_t* sA = smem + s * NN_STAGE_BYTES;
+          uint8_t* sB = sA + NN_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], NN_STAGE_BYTES);
+          const int k = kt * BK;
+#pragma unroll
+          for (int mb = 0; mb < BM / 16; ++mb)
+            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+          tma_load_2d(sB, &mapB, k, n_tile * NN_BN, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2;
+  const int q = lane & 3;
+  const int m0 = (warp & 3) * 32;
+  const int n0 = (warp >> 2) * (NN_BN / 2);
+  int kit = 0, it = 0;
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    int m_tile, n_tile;
+    decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+    const int cb = it & 1;
+    const int mg0 = m_tile * BM;
+    const int ng0 = n_tile * NN_BN;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < num_k; ++kt, ++kit) {
+      const int s = kit % STAGES;
+      mbar_wait(&full[s], (kit / STAGES) & 1);
+      const uint8_t* sA = smem + s * NN_STAGE_BYTES;
+      const uint8_t* sB = sA + NN_A_BYTES;
+      const int kg0 = kt * BK;
+      if (args.mask_a && mg0 <= kg0 + BK - 1)
+        consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else
+        consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // epilogue: C_smem -= acc, then one TMA store of the tile
+    mbar_wait(&cfull[cb], (it >> 1) & 1);
+    uint8_t* cbuf = cbuf0 + cb * NN_C_BYTES;
+#pragma unroll
+    for (int mp = 0; mp < 2; ++mp) {
+      const int m = m0 + mp * 16 + 2 * g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + nt * 8 + 2 * q + e;
+          double2* p = reinterpret_cast<double2*>(cbuf + n * (BM * 8) + m * 8);
+          double2 c = *p;
+          c.x -= acc[mp * 2 + 0][nt][e];
+          c.y -= acc[mp * 2 + 1][nt][e];
+          *p = c;
+        }
+      }
+    }
+    fence_proxy_async();
+    named_bar_sync(1, CONSUMER_WARPS * 32);
+    if (threadIdx.x == 0) {
+      tma_store_2d(&mapC, cbuf, mg0, ng0);
+      bulk_commit();
+      bulk_wait_read0();
+      mbar_arrive(&cempty[cb]);
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -296,7 +455,8 @@ int get_encoder() {
   return QRB_OK;
 }
 
-int make_map(CUtensorMap* map, const MatView& v, uint32_t box_rows, uint32_t box_cols) {
+int make_map(CUtensorMap* map, const MatView& v, uint32_t box_rows, uint32_t box_cols,
+             bool swizzle = true) {
   QRB_TRY(get_encoder());
   if (v.rows < 1 || v.cols < 1) {
     set_last_error("make_map: empty view");
@@ -311,7 +471,8 @@ int make_map(CUtensorMap* map, const MatView& v, uint32_t box_rows, uint32_t box
   cuuint32_t box[2] = {box_rows, box_cols};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, v.ptr, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_last_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -416,6 +577,31 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   if ((reinterpret_cast<uintptr_t>(out) & 15) != 0 || (ldo & 1) != 0) {
     set_last_error("gemm_nn: output must be 16-byte aligned with even ld");
     return QRB_ERR_ARG;
+  }
+  if (epi == GEMM_EPI_SUB && !(std::getenv("QRB_NN_CLASSIC"))) {
+    static bool configured = false;
+    if (!configured) {
+      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_persistent,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, NN_SMEM));
+      configured = true;
+    }
+    CUtensorMap ma, mb, mc;
+    QRB_TRY(make_map(&ma, a_mm, 16, BK));
+    QRB_TRY(make_map(&mb, b, BK, NN_BN));
+    QRB_TRY(make_map(&mc, MatView{out, M, N, ldo}, BM, NN_BN, false));
+    NnArgs args;
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.mask_a = mask_a;
+    args.group_m = 16;
+    const int num_m = (M + BM - 1) / BM;
+    const int num_n = (N + NN_BN - 1) / NN_BN;
+    args.num_tiles = num_m * num_n;
+    const int grid = std::min(args.num_tiles, gemm_sm_count());
+    gemm_nn_sub_persistent<<<grid, THREADS, NN_SMEM, stream>>>(ma, mb, mc, args);
+    QRB_CUDA_TRY(cudaGetLastError());
+    return QRB_OK;
   }
   if (epi == GEMM_EPI_SUB)
     return launch<false, 64, GEMM_EPI_SUB>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
