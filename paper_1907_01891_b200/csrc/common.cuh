@@ -156,7 +156,6 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     unsigned int v;
     do {

@@ -56,6 +56,14 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return static_cast<uint32_t>(row * 128 + (((chunk ^ (row & 7)) & 7) << 4));
 }
 
+// Fragment row permutation for K-major operands.  An LDS.128 is served per
+// quarter-warp (8 lanes = fragment rows g in {2k, 2k+1}); mapping fragment row g
+// to tile row RP(g) = [0,5,2,7,4,1,6,3][g] makes those two rows differ in bit 2,
+// so the 128B-swizzled chunks of the 8 lanes are distinct (no bank conflicts),
+// and even / odd output columns land on even / odd swizzle rows, which keeps
+// the swizzled C-tile epilogue conflict-free as well.
+__device__ __forceinline__ int rp(int g) { return (g & 6) ^ ((g & 1) * 5); }
+
 // unit-lower-trapezoid masking of a pair of consecutive view rows (r, r+1) at view column c
 __device__ __forceinline__ void mask_pair(double2& v, int r, int c) {
   if (r <= c) v.x = (r == c) ? 1.0 : 0.0;
@@ -72,14 +80,14 @@ __device__ __forceinline__ void consume_stage(double (&acc)[4][BN / 16][2], cons
     double2 b[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const int row = n0 + nt * 8 + g;
+      const int row = n0 + nt * 8 + rp(g);
       b[nt] = *reinterpret_cast<const double2*>(sB + swz(row, (kc >> 1) + q));
       if constexpr (MASK_B) mask_pair(b[nt], kg0 + kc + 2 * q, ng0 + row);
     }
     if constexpr (A_KMAJOR) {
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const int row = m0 + mt * 8 + g;
+        const int row = m0 + mt * 8 + rp(g);
         double2 a = *reinterpret_cast<const double2*>(sA + swz(row, (kc >> 1) + q));
         if constexpr (MASK_A) mask_pair(a, kg0 + kc + 2 * q, mg0 + row);
 #pragma unroll
@@ -221,15 +229,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   if constexpr (A_KMAJOR) {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
-      const int m = mg0 + m0 + mt * 8 + g;
+      const int m = mg0 + m0 + mt * 8 + rp(g);
       if (m >= args.M) continue;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const int n = ng0 + n0 + nt * 8 + 2 * q;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (n + e < args.N) {
-            double* p = out + m + static_cast<int64_t>(n + e) * ldo;
+          const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
+          if (n < args.N) {
+            double* p = out + m + static_cast<int64_t>(n) * ldo;
             if constexpr (EPI == GEMM_EPI_SUB)
               *p -= acc[mt][nt][e];
             else
@@ -246,11 +254,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool pair = (m + 1 < args.M);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const int n = ng0 + n0 + nt * 8 + 2 * q;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (n + e >= args.N) continue;
-          double* p = out + m + static_cast<int64_t>(n + e) * ldo;
+          const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
+          if (n >= args.N) continue;
+          double* p = out + m + static_cast<int64_t>(n) * ldo;
           const double v0 = acc[mp * 2 + 0][nt][e];
           const double v1 = acc[mp * 2 + 1][nt][e];
           if (pair) {
@@ -355,7 +363,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int cb = it & 1;
         if (it >= 2) mbar_wait(&cempty[cb], ((it >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&cfull[cb], NN_C_BYTES);
-        tma_load_2d(cbuf0 + cb * NN_C_BYTES, &mapC, m_tile * BM, n_tile * NN_BN, &cfull[cb]);
+#pragma unroll
+        for (int mb = 0; mb < BM / 16; ++mb)
+          tma_load_2d(cbuf0 + cb * NN_C_BYTES + mb * (NN_BN * 128), &mapC, m_tile * BM + mb * 16,
+                      n_tile * NN_BN, &cfull[cb]);
         for (int kt = 0; kt < num_k; ++kt, ++kit) {
           const int s = kit % STAGES;
           if (kit >= STAGES) mbar_wait(&empty[s], ((kit / STAGES) & 1) ^ 1);
@@ -412,8 +423,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int n = n0 + nt * 8 + 2 * q + e;
-          double2* p = reinterpret_cast<double2*>(cbuf + n * (BM * 8) + m * 8);
+          const int n = n0 + nt * 8 + rp(2 * q + e);
+          // swizzled [16-row block][64 cols][16 rows] staging (TMA SWIZZLE_128B)
+          double2* p = reinterpret_cast<double2*>(cbuf + (m >> 4) * (NN_BN * 128) +
+                                                  swz(n, (m & 15) >> 1));
           double2 c = *p;
           c.x -= acc[mp * 2 + 0][nt][e];
           c.y -= acc[mp * 2 + 1][nt][e];
@@ -424,7 +437,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_proxy_async();
     named_bar_sync(1, CONSUMER_WARPS * 32);
     if (threadIdx.x == 0) {
-      tma_store_2d(&mapC, cbuf, mg0, ng0);
+#pragma unroll
+      for (int mb = 0; mb < BM / 16; ++mb)
+        tma_store_2d(&mapC, cbuf + mb * (NN_BN * 128), mg0 + mb * 16, ng0);
       bulk_commit();
       bulk_wait_read0();
       mbar_arrive(&cempty[cb]);
@@ -588,7 +603,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     CUtensorMap ma, mb, mc;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
-    QRB_TRY(make_map(&mc, MatView{out, M, N, ldo}, BM, NN_BN, false));
+    QRB_TRY(make_map(&mc, MatView{out, M, N, ldo}, 16, NN_BN));
     NnArgs args;
     args.M = M;
     args.N = N;

@@ -22,6 +22,8 @@
 #include "panel.h"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace qrb {
 
@@ -37,11 +39,16 @@ struct PanelArgs {
   int ib;
   int R;  // rows per CTA
   double* tau;
-  double* G;  // ib x ib, ld = ib
+  double* G;  // ib x ib, ld = ldg
   int ldg;
-  double* part;  // [P][ib + 2] partial sums, then scalar slots
+  double* part;  // 2 x [(ib + 1) * P + ib] partial sums / pivot-row slots
   unsigned int* bar;
+  unsigned long long* trace;  // optional per-phase timing (QRB_PANEL_TRACE)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  return clock64();
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -49,31 +56,24 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// deterministic block sum; result valid in all threads
-__device__ double block_sum(double v, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (warp == 0) {
-    s = lane < PANEL_WARPS ? red[lane] : 0.0;
-    s = warp_sum(s);
-    if (lane == 0) red[PANEL_WARPS] = s;
-  }
-  __syncthreads();
-  return red[PANEL_WARPS];
-}
-
+// One grid-wide reduction per column.  For column j with x = a[j+1:, j]
+// (not yet scaled) every CTA publishes, over its own rows r > j,
+//     sigma_p = sum x_r^2          d'_p[c] = sum x_r a[r][c]   (all c != j)
+// and the CTA owning row j publishes that row.  After one grid barrier all
+// CTAs derive beta, tau, scale = 1/(alpha - beta) and
+//     d[c] = a[j][c] + scale * sum_p d'_p[c]  = v_j^T a[:, c]
+// which is the rank-1 update row for c > j (kernels.py:97-100) and the Gram
+// entry V[:, c]^T v_j of the T recurrence for c < j (kernels.py:143-146).
+// Partial buffers alternate by column parity, so a CTA that races ahead into
+// column j+1 never overwrites partials another CTA is still summing.
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p) {
   extern __shared__ double smem_d[];
   const int R = p.R;
   const int ib = p.ib;
   double* slab = smem_d;                 // ib columns x R rows, column-major
-  double* dsum = slab + (size_t)ib * R;  // ib reduced dot products
-  double* red = dsum + ib;               // PANEL_WARPS + 1
-  double* scal = red + PANEL_WARPS + 2;  // tau, scale, beta, skip
+  double* red = slab + (size_t)ib * R;   // ib reduced sums
+  double* rowj = red + ib;               // ib pivot-row values
+  double* scal = rowj + ib;              // tau, scale, beta, skip
 
   const int P = gridDim.x;
   const int cta = blockIdx.x;
@@ -81,9 +81,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
   const int warp = tid >> 5, lane = tid & 31;
   const int r0 = cta * R;
   const int nrows = max(0, min(R, p.m - r0));
-  const int stride = ib + 2;
-  double* my_part = p.part + (size_t)cta * stride;
-  double* alpha_slot = p.part + (size_t)P * stride;
+  const size_t buf_stride = (size_t)(ib + 1) * P + ib + 8;
   unsigned int nbar = 0;
 
   for (int idx = tid; idx < ib * R; idx += PANEL_THREADS) {
@@ -92,117 +90,169 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
   }
   __syncthreads();
 
-  // partial norm of column 0 below the diagonal
-  double nrm = 0.0;
-  for (int lr = tid; lr < nrows; lr += PANEL_THREADS) {
-    if (r0 + lr > 0) {
-      const double x = slab[lr];
-      nrm += x * x;
-    }
-  }
-  nrm = block_sum(nrm, red);
-
-  const int tpc = PANEL_THREADS / ib;  // threads per column in the dot reduction
-
+  unsigned long long tph[5] = {0, 0, 0, 0, 0};
+  const bool tracing = p.trace != nullptr && tid == 0;
+  // column c is owned by warp c % PANEL_WARPS: that warp computes its partial
+  // sums, reduces its w_c after the barrier and applies its rank-1 update, so
+  // the only intra-CTA synchronisation per column is one __syncthreads.
+  constexpr int OWN = 8;  // columns per warp (ib <= 128)
+  constexpr int MAXB = 5;  // partial loads per lane (P <= 160)
   for (int j = 0; j < ib; ++j) {
-    const int lj = j - r0;  // local index of the diagonal row (may be out of slab)
-    if (tid == 0) {
-      my_part[0] = nrm;
-      if (lj >= 0 && lj < nrows) *alpha_slot = slab[(size_t)j * R + lj];
+    unsigned long long ta = tracing ? gtimer() : 0, tb = 0;
+    double* part = p.part + (size_t)(j & 1) * buf_stride;  // [c * P + cta]
+    double* prow = part + (size_t)(ib + 1) * P;             // pivot row j
+    const int lj = j - r0;
+    const bool owner = lj >= 0 && lj < nrows;
+    double* x = slab + (size_t)j * R;
+    const int lstart = max(0, lj + 1);
+
+    // ---- local partial sums over this slab's rows r > j ----
+    {
+      double acc[OWN];
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) acc[i] = 0.0;
+      for (int lr = lstart + lane; lr < nrows; lr += 32) {
+        const double xv = x[lr];
+#pragma unroll
+        for (int i = 0; i < OWN; ++i) {
+          const int c = warp + i * PANEL_WARPS;
+          if (c < ib) acc[i] += xv * slab[(size_t)c * R + lr];
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < OWN; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      if (lane < OWN) {
+        double v = acc[0];
+#pragma unroll
+        for (int i = 1; i < OWN; ++i)
+          if (lane == i) v = acc[i];
+        const int c = warp + lane * PANEL_WARPS;
+        if (c < ib) part[(size_t)c * P + cta] = v;  // c == j holds sigma
+      }
+    }
+    if (owner)
+      for (int c = tid; c < ib; c += PANEL_THREADS) prow[c] = slab[(size_t)c * R + lj];
+    if (tracing) {
+      tb = gtimer();
+      tph[0] += tb - ta;
+      ta = tb;
     }
     grid_barrier(p.bar, (++nbar) * P);
+    if (tracing) {
+      tb = gtimer();
+      tph[1] += tb - ta;
+      ta = tb;
+    }
 
-    if (warp == 0) {
-      double s = 0.0;
-      for (int c = lane; c < P; c += 32) s += __ldcg(p.part + (size_t)c * stride);
-      s = warp_sum(s);
-      if (lane == 0) {
-        const double alpha = __ldcg(alpha_slot);
-        if (s == 0.0) {
-          scal[0] = 0.0;
-          scal[3] = 1.0;
-        } else {
-          const double beta = -copysign(sqrt(alpha * alpha + s), alpha);
-          scal[0] = (beta - alpha) / beta;
-          scal[1] = 1.0 / (alpha - beta);
-          scal[2] = beta;
-          scal[3] = 0.0;
+    // ---- every warp re-sums sigma and its own columns' partials (fixed order) ----
+    double red_i[OWN], row_i[OWN];
+    double sigma, alpha;
+    {
+      // warp 0 alone fetches sigma / alpha (one reader per CTA for the hot line)
+      if (warp == 0) {
+        const double* src = part + (size_t)j * P;
+        double t = 0.0;
+        for (int b = lane; b < P; b += 32) t += __ldcg(src + b);
+        t = warp_sum(t);
+        if (lane == 0) {
+          scal[0] = t;
+          scal[1] = __ldcg(prow + j);
         }
       }
-    }
-    __syncthreads();
-    const bool skip = scal[3] != 0.0;
-    double* vcol = slab + (size_t)j * R;
-    const int lstart = max(0, lj);  // first local row with global row >= j
-
-    if (!skip) {
-      const double sc = scal[1];
-      for (int lr = max(0, lj + 1) + tid; lr < nrows; lr += PANEL_THREADS) vcol[lr] *= sc;
+      double v[OWN][MAXB];
+      double rv[OWN];
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        const int c = warp + i * PANEL_WARPS;
+        const bool need = c < ib && (c > j || (cta == 0 && c < j));
+        const double* src = part + (size_t)c * P;
+#pragma unroll
+        for (int k = 0; k < MAXB; ++k) {
+          const int b = lane + 32 * k;
+          v[i][k] = (need && b < P) ? __ldcg(src + b) : 0.0;
+        }
+        rv[i] = (need && lane == i) ? __ldcg(prow + c) : 0.0;
+      }
+      double sm[OWN];
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXB; ++k) t += v[i][k];
+        sm[i] = t;
+      }
+      if (tracing) {
+        double guard = 0.0;
+#pragma unroll
+        for (int i = 0; i < OWN; ++i) guard += sm[i] + rv[i];
+        tb = gtimer() + (guard == 12345.678 ? 1 : 0);
+        tph[4] += tb - ta;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < OWN; ++i) sm[i] += __shfl_xor_sync(0xffffffffu, sm[i], o);
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        red_i[i] = sm[i];
+        row_i[i] = __shfl_sync(0xffffffffu, rv[i], i);
+      }
       __syncthreads();
-      // partial dots of v_j (unit at row j) with every other panel column
-      for (int c = warp; c < ib; c += PANEL_WARPS) {
-        if (c == j) continue;
-        const double* col = slab + (size_t)c * R;
-        double s = 0.0;
-        for (int lr = lstart + lane; lr < nrows; lr += 32) {
-          const double v = (lr == lj) ? 1.0 : vcol[lr];
-          s += col[lr] * v;
+      sigma = scal[0];
+      alpha = scal[1];
+    }
+    const bool skip = sigma == 0.0;
+    double tau = 0.0, sc = 0.0, beta = 0.0;
+    if (!skip) {
+      beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
+      tau = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    if (tracing) {
+      tb = gtimer();
+      tph[2] += tb - ta;
+      ta = tb;
+    }
+    if (cta == 0) {
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        const int c = warp + i * PANEL_WARPS;
+        if (c < j && lane == i) p.G[c + (int64_t)j * p.ldg] = skip ? 0.0 : row_i[i] + sc * red_i[i];
+      }
+      if (tid == 0) p.tau[j] = tau;
+    }
+    if (!skip) {
+      // rank-1 update of the owned columns c > j on rows >= j of this slab
+      const int lfirst = max(0, lj);
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        const int c = warp + i * PANEL_WARPS;
+        if (c > j && c < ib) {
+          const double srow = tau * (row_i[i] + sc * red_i[i]);
+          double* col = slab + (size_t)c * R;
+          for (int lr = lfirst + lane; lr < nrows; lr += 32) {
+            const double vv = (lr == lj) ? 1.0 : x[lr] * sc;
+            col[lr] -= vv * srow;
+          }
         }
-        s = warp_sum(s);
-        if (lane == 0) my_part[1 + c] = s;
-      }
-      grid_barrier(p.bar, (++nbar) * P);
-      // every CTA re-sums the partial dots in a fixed order
-      {
-        const int c = tid % ib;
-        const int sub = tid / ib;
-        double s = 0.0;
-        if (sub < tpc)
-          for (int b = sub; b < P; b += tpc) s += __ldcg(p.part + (size_t)b * stride + 1 + c);
-        // combine the tpc sub-sums through shared memory in fixed order
-        double* tmp = slab + (size_t)ib * R + ib + PANEL_WARPS + 8;  // scratch after scal
-        if (sub < tpc) tmp[sub * ib + c] = s;
-        __syncthreads();
-        if (tid < ib) {
-          double t = 0.0;
-          for (int u = 0; u < tpc; ++u) t += tmp[u * ib + tid];
-          dsum[tid] = t;
-        }
-        __syncthreads();
-      }
-      const double tau = scal[0];
-      if (cta == 0) {
-        if (tid < j) p.G[tid + (int64_t)j * p.ldg] = dsum[tid];
-        if (tid == 0) p.tau[j] = tau;
-      }
-      // rank-1 update of the columns right of j (rows >= j in this slab)
-      const int ncol = ib - j - 1;
-      const int nr = nrows - lstart;
-      if (ncol > 0 && nr > 0) {
-        for (int idx = tid; idx < ncol * nr; idx += PANEL_THREADS) {
-          const int cc = idx / nr;
-          const int lr = lstart + (idx - cc * nr);
-          const int c = j + 1 + cc;
-          const double srow = tau * dsum[c];
-          const double v = (lr == lj) ? 1.0 : vcol[lr];
-          slab[(size_t)c * R + lr] -= v * srow;
-        }
-      }
-      if (tid == 0 && lj >= 0 && lj < nrows) vcol[lj] = scal[2];
-    } else {
-      if (cta == 0) {
-        if (tid < j) p.G[tid + (int64_t)j * p.ldg] = 0.0;
-        if (tid == 0) p.tau[j] = 0.0;
       }
     }
     __syncthreads();
-    if (j + 1 < ib) {
-      const double* col = slab + (size_t)(j + 1) * R;
-      double s = 0.0;
-      for (int lr = tid; lr < nrows; lr += PANEL_THREADS)
-        if (r0 + lr > j + 1) s += col[lr] * col[lr];
-      nrm = block_sum(s, red);
+    if (!skip && warp == (j % PANEL_WARPS)) {
+      // the owner warp turns column j into the reflector (and beta on the diagonal)
+      for (int lr = lstart + lane; lr < nrows; lr += 32) x[lr] *= sc;
+      if (owner && lane == 0) x[lj] = beta;
+      __syncwarp();
     }
+    if (tracing) tph[3] += gtimer() - ta;
+  }
+  __syncthreads();
+  if (tracing && (cta == 0 || cta == P - 1)) {
+    unsigned long long* t = p.trace + (cta == 0 ? 0 : 4);
+    for (int i = 0; i < 4; ++i) atomicAdd(t + i, tph[i]);
+    if (cta == 0) atomicAdd(p.trace + 8, tph[4]);
   }
 
   for (int idx = tid; idx < ib * R; idx += PANEL_THREADS) {
@@ -309,7 +359,7 @@ int panel_max_ctas() {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cap = sms > 0 ? sms : 148;
+    cap = sms > 0 ? (sms < 160 ? sms : 160) : 148;  // reduce loop handles P <= 160
   }
   return cap;
 }
@@ -325,7 +375,7 @@ PanelPlan panel_plan(int m, int w_max) {
   P = (m + R - 1) / R;
   const size_t budget = 200 * 1024;
   int ib = 128;
-  while (ib > 8 && (size_t)ib * R * 8 + (size_t)ib * 8 * (PANEL_THREADS / ib + 1) > budget) ib >>= 1;
+  while (ib > 8 && panel_smem_bytes(R, ib) > budget) ib >>= 1;
   if (ib > w_max) ib = w_max;
   pl.P = P;
   pl.R = R;
@@ -334,9 +384,10 @@ PanelPlan panel_plan(int m, int w_max) {
 }
 
 size_t panel_smem_bytes(int R, int ib) {
-  const int tpc = PANEL_THREADS / ib;
-  return ((size_t)ib * R + ib + PANEL_WARPS + 8 + (size_t)tpc * ib + 8) * sizeof(double);
+  return ((size_t)ib * R + 2 * (size_t)ib + 8) * sizeof(double);
 }
+
+size_t panel_part_doubles(int P, int ib) { return 2 * ((size_t)(ib + 1) * P + ib + 8); }
 
 int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int ldg,
                  double* part, unsigned int* bar, cudaStream_t stream) {
@@ -369,9 +420,36 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
   a.ldg = ldg;
   a.part = part;
   a.bar = bar;
+  a.trace = nullptr;
+  static unsigned long long* trace_buf = nullptr;
+  static bool trace_on = std::getenv("QRB_PANEL_TRACE") != nullptr;
+  if (trace_on) {
+    if (!trace_buf) {
+      QRB_CUDA_TRY(cudaMallocManaged(&trace_buf, 16 * sizeof(unsigned long long)));
+      for (int i = 0; i < 16; ++i) trace_buf[i] = 0;
+    }
+    a.trace = trace_buf;
+  }
   void* args[] = {&a};
   QRB_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(panel_qr_kernel), dim3(P),
                                            dim3(PANEL_THREADS), args, smem, stream));
+  if (trace_on) {
+    static int calls = 0;
+    static double cols_total = 0;
+    QRB_CUDA_TRY(cudaStreamSynchronize(stream));
+    cols_total += ib;
+    if (++calls % 64 == 0)
+      std::fprintf(stderr,
+                   "[panel trace] %d calls, %.0f cols: per column (kcycles) cta0 local %.2f barrier "
+                   "%.2f reduce %.2f (loads %.2f) update %.2f | last cta local %.2f barrier %.2f "
+                   "reduce %.2f update %.2f\n",
+                   calls, cols_total, trace_buf[0] / cols_total / 1e3,
+                   trace_buf[1] / cols_total / 1e3, trace_buf[2] / cols_total / 1e3,
+                   trace_buf[8] / cols_total / 1e3,
+                   trace_buf[3] / cols_total / 1e3, trace_buf[4] / cols_total / 1e3,
+                   trace_buf[5] / cols_total / 1e3, trace_buf[6] / cols_total / 1e3,
+                   trace_buf[7] / cols_total / 1e3);
+  }
   return QRB_OK;
 }
 

@@ -12,6 +12,7 @@ struct PanelPlan {
 
 PanelPlan panel_plan(int m, int w_max);
 size_t panel_smem_bytes(int R, int ib);
+size_t panel_part_doubles(int P, int ib);
 int panel_max_ctas();
 
 // Householder QR of an m x w panel in place (R on/above the diagonal, unit-lower

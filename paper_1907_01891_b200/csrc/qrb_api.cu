@@ -214,7 +214,7 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
   QRB_TRY(ws.Ti.ensure(sizeof(double) * 128 * 128, st));
   QRB_TRY(ws.bar.ensure(64, st));
   PanelPlan pl = panel_plan(m, pw);
-  QRB_TRY(ws.part.ensure(sizeof(double) * ((size_t)(pl.P + 1) * (128 + 2) + 64), st));
+  QRB_TRY(ws.part.ensure(sizeof(double) * panel_part_doubles(panel_max_ctas(), 128), st));
   unsigned int* bar = static_cast<unsigned int*>(ws.bar.p);
   if (pl.ib >= pw) {
     QRB_TRY(panel_factor(panel, pl.P, pl.R, tau, ws.G.d(), ldg, ws.part.d(), bar, st));

@@ -1,0 +1,13 @@
+import sys, ctypes, os
+import numpy as np, torch
+sys.path.insert(0, ".")
+from paper_1907_01891_b200 import _native
+lib = _native.load()
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+m = int(sys.argv[1]); w = 128
+A = torch.randn(w, m, dtype=torch.float64, device="cuda")
+tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+T = torch.zeros(w, w, dtype=torch.float64, device="cuda")
+for _ in range(64):
+    lib.qrb_op_panel(P(A), m, m, w, P(tau), P(T), w, None)
+torch.cuda.synchronize()
