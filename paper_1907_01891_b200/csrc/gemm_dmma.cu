@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // keep the pointer derived from the __shared__ array so loads compile to LDS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                            const __grid_constant__ CUtensorMap mapC, const NnArgs args) {
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // keep the pointer derived from the __shared__ array so loads compile to LDS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* cbuf0 = smem + STAGES * NN_STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(cbuf0 + 2 * NN_C_BYTES);
   uint64_t* empty = full + STAGES;
@@ -553,7 +553,7 @@ int gemm_sm_count() {
 // the machine with little wave quantization
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
   const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
-  const int slots = 2 * gemm_sm_count();
+  const int slots = gemm_sm_count();  // one 288-thread CTA per SM (168 regs)
   const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
   int best = 1;
   double best_eff = 0.0;
