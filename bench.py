@@ -184,7 +184,7 @@ def ours_arm(args, rank: int, world: int):
     from paper_1907_01891_b200 import ct_system as cs
     from paper_1907_01891_b200.device import QrDevice, launch_count
 
-    if world > 1:
+    if world > 1 or args.force_dist:
         from paper_1907_01891_b200 import dist
         return dist.bench_rank(args, rank, world)
 
@@ -260,6 +260,8 @@ def ours_arm(args, rank: int, world: int):
     x_last = x_dev[:, :n]
     r_explicit = torch.linalg.norm(x_last @ a_dev[:, :m] - b_dev[:, :m], dim=1)
     resid_rel = float((torch.abs(r_explicit - r_dev) / r_explicit).max())
+    resid_dbg = {"explicit": r_explicit[:3].tolist(), "identity": r_dev[:3].tolist(),
+                 "x_absmax": float(x_last.abs().max())}
 
     # end-to-end through the public host API (pinned host A and B, host X out)
     a_pin = torch.empty((n, lda), dtype=torch.float64, pin_memory=True)
@@ -316,7 +318,7 @@ def ours_arm(args, rank: int, world: int):
                          "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
                                    f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
-        "check": {"resid_identity_max_rel": resid_rel},
+        "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s,
     }
     print(json.dumps(line), flush=True)
@@ -332,6 +334,8 @@ def main():
     ap.add_argument("--nb", type=int, default=128)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

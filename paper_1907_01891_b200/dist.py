@@ -1,0 +1,288 @@
+"""Multi-GPU factorization and solve: one process per GPU, torch.distributed.
+
+Layout (BASELINE.json north_star): the m x n matrix is split 1D block-cyclic
+by column panels of width nb -- panel k lives on rank k % G as local panel
+k // G, local panels stored contiguously (column-major, leading dim lda).
+
+Factorization, step k (j0 = k nb, m_k = m - j0):
+  1. the owner factors panel k in place (qrb_op_panel: geqr2 + T);
+  2. the owner packs (V_k, T_k) into one contiguous buffer and broadcasts it
+     (NCCL over NVLink/NVSwitch on the GPU box; gloo in the CPU tests) --
+     the single exchange of the step;
+  3. every rank applies Q_k^T to its local panels with index > k
+     (qrb_op_apply_qt: the DMMA trailing update).
+The reference has no distributed code; its analogue of
+scaling past one device is the out-of-core tile schedule (task_engine.py:187-217).
+
+Solve: slices are independent, so after the factorization the factored
+panels and the T factors are all-gathered once and every rank solves its
+share of the slices against a full resident copy (no communication during
+the solve).
+
+The per-step local arithmetic is injected (``ops``): the product uses
+:class:`CudaOps` (the sm_100a library); the CPU tests inject numpy ops to check
+the distributed schedule itself over gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def owner_of(k: int, world: int) -> int:
+    return k % world
+
+
+def local_panels(npanels: int, rank: int, world: int) -> list[int]:
+    """Global indices of the panels rank owns, in local storage order."""
+    return list(range(rank, npanels, world))
+
+
+def local_cols(n: int, nb: int, rank: int, world: int) -> int:
+    npan = -(-n // nb)
+    return sum(min(nb, n - k * nb) for k in local_panels(npan, rank, world))
+
+
+def first_local_after(k: int, rank: int, world: int) -> int:
+    """Local panel index of the first owned panel with global index > k."""
+    if rank > k:
+        return 0
+    return (k - rank) // world + 1
+
+
+class CudaOps:
+    """Local arithmetic through the C ABI (stream-ordered qrb_op_* calls on
+    torch CUDA tensors holding column-major matrices as (cols, ld) tensors)."""
+
+    def __init__(self):
+        from . import _native
+        self.lib = _native.load()
+        self.native = _native
+
+    @staticmethod
+    def _p(t, off=0):
+        return ctypes.c_void_p(t.data_ptr() + 8 * off)
+
+    def panel(self, a, lda, row0, col0, m, w, tau, t, ldt):
+        st = self.lib.qrb_op_panel(self._p(a, row0 + col0 * lda), lda, m, w, self._p(tau),
+                                   self._p(t), ldt, None)
+        self.native.check(st, "qrb_op_panel")
+
+    def apply_qt(self, v, ldv, v_off, m, w, t, ldt, c, ldc, c_off, nc):
+        if nc <= 0:
+            return
+        st = self.lib.qrb_op_apply_qt(self._p(v, v_off), ldv, m, w, self._p(t), ldt,
+                                      self._p(c, c_off), ldc, nc, None)
+        self.native.check(st, "qrb_op_apply_qt")
+
+    def sync(self):
+        import torch
+        torch.cuda.synchronize()
+
+
+@dataclass
+class DistFactors:
+    m: int
+    n: int
+    nb: int
+    lda: int
+    rank: int
+    world: int
+    a_local: object                     # torch (n_local, lda): factored local panels
+    t_all: object                       # torch (npanels*nb, nb): T_k of every panel (rows = T columns)
+    tau_all: object = None
+    factor_seconds: float = 0.0
+    stats: dict = field(default_factory=dict)
+
+
+def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int, world: int,
+                          ops, group=None) -> DistFactors:
+    """Blocked Householder QR of the block-cyclic matrix; a_local is overwritten
+    with the local panels of the factored matrix (R above, V below)."""
+    import torch
+    import torch.distributed as dist
+
+    npan = -(-n // nb)
+    dev = a_local.device
+    dt = torch.float64
+    t_all = torch.zeros((npan * nb, nb), dtype=dt, device=dev)
+    tau_all = torch.zeros(npan * nb, dtype=dt, device=dev)
+    ldv_max = m + (m & 1)
+    buf = torch.empty(ldv_max * nb + nb * nb + nb, dtype=dt, device=dev)
+    n_local = a_local.shape[0]
+    bytes_bcast = 0
+    ops.sync()
+    t0 = time.perf_counter()
+    for k in range(npan):
+        j0 = k * nb
+        pw = min(nb, n - j0)
+        mk = m - j0
+        ldv = mk + (mk & 1)
+        root = owner_of(k, world)
+        nelem = ldv * pw + nb * nb + nb
+        vview = buf[: ldv * pw].view(pw, ldv)
+        tview = buf[ldv * pw: ldv * pw + nb * nb].view(nb, nb)
+        tauv = buf[ldv * pw + nb * nb: nelem]
+        if rank == root:
+            lcol = (k // world) * nb
+            tview.zero_()
+            ops.panel(a_local, lda, j0, lcol, mk, pw, tauv, tview, nb)
+            vview[:, :mk].copy_(a_local[lcol:lcol + pw, j0:m])
+        if world > 1:
+            dist.broadcast(buf[:nelem], src=root, group=group)
+            bytes_bcast += 8 * nelem
+        t_all[k * nb:(k + 1) * nb].copy_(tview)
+        tau_all[j0:j0 + pw].copy_(tauv[:pw])
+        lfirst = first_local_after(k, rank, world) * nb
+        ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, a_local, lda, j0 + lfirst * lda,
+                     n_local - lfirst)
+    ops.sync()
+    secs = time.perf_counter() - t0
+    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs,
+                       {"bytes_broadcast": bytes_bcast, "panels": npan})
+
+
+def gather_factored(f: DistFactors, group=None, place=None):
+    """All ranks receive every factored panel.  With ``place(k, panel)`` each
+    (pw, lda) panel view is handed to the caller (e.g. copied straight into a
+    QrDevice); otherwise the full (n, lda) tensor is returned."""
+    import torch
+    import torch.distributed as dist
+
+    npan = -(-f.n // f.nb)
+    max_local = max(local_cols(f.n, f.nb, r, f.world) for r in range(f.world))
+    dev = f.a_local.device
+    send = torch.zeros((max_local, f.lda), dtype=torch.float64, device=dev)
+    send[: f.a_local.shape[0]].copy_(f.a_local)
+    if f.world > 1:
+        recv = torch.empty((f.world * max_local, f.lda), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:
+        recv = send
+    full = None if place else torch.empty((f.n, f.lda), dtype=torch.float64, device=dev)
+    for k in range(npan):
+        r, lk = owner_of(k, f.world), k // f.world
+        pw = min(f.nb, f.n - k * f.nb)
+        src = recv[r * max_local + lk * f.nb: r * max_local + lk * f.nb + pw]
+        if place:
+            place(k, src)
+        else:
+            full[k * f.nb:k * f.nb + pw].copy_(src)
+    return full
+
+
+def scatter_block_cyclic(a_full_cols, n: int, nb: int, rank: int, world: int):
+    """This rank's local panels (torch (n_local, lda)) from a full (n, lda) tensor."""
+    import torch
+    npan = -(-n // nb)
+    parts = [a_full_cols[k * nb:min(n, (k + 1) * nb)] for k in local_panels(npan, rank, world)]
+    if not parts:
+        return a_full_cols[:0].clone()
+    return torch.cat(parts, dim=0).contiguous()
+
+
+def slice_share(s: int, rank: int, world: int) -> tuple[int, int]:
+    """[first, count) of the slices this rank solves."""
+    base, rem = divmod(s, world)
+    first = rank * base + min(rank, rem)
+    return first, base + (1 if rank < rem else 0)
+
+
+# -- benchmark rank (bench.py under torchrun) -----------------------------------------------
+
+
+def bench_rank(args, rank: int, world: int):
+    import json
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local_rank))
+    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload,
+                       densify_device, qr_flops, solve_flops)
+    from . import ct_system as cs
+    from .device import QrDevice, launch_count
+
+    g, coo, x_true, S = build_workload(args.config, args.slices)
+    m, n, nb = g.n_rays, g.n_pixels, args.nb
+    lda = (m + 31) // 32 * 32
+    a_full = densify_device(g, coo, lda)
+    xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()
+    b_host = cs.noisy_sinograms((xt @ a_full[:, :m]).cpu().numpy().T, args.config)
+    a_pristine = scatter_block_cyclic(a_full, n, nb, rank, world)
+    del a_full, xt
+    torch.cuda.empty_cache()
+    first, cnt = slice_share(S, rank, world)
+    b_dev = torch.zeros((max(cnt, 1), lda), dtype=torch.float64, device="cuda")
+    b_dev[:cnt, :m] = torch.from_numpy(np.ascontiguousarray(b_host[:, first:first + cnt].T)).cuda()
+    x_dev = torch.zeros((max(cnt, 1), n + (n & 1)), dtype=torch.float64, device="cuda")
+    ops = CudaOps()
+    a_local = torch.empty_like(a_pristine)
+    q = QrDevice(m, n, nb)
+
+    def step():
+        a_local.copy_(a_pristine)
+        f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
+        t1 = time.perf_counter()
+        gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
+        q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+        t2 = time.perf_counter()
+        srep = q.solve_device(b_dev[:cnt], x_dev[:cnt]) if cnt else {"total_ms": 0.0}
+        return f.factor_seconds, t2 - t1, srep["total_ms"] / 1e3
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    l0 = launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fs, gs, ss = [], [], []
+    for _ in range(args.steps):
+        a, b, c = step()
+        fs.append(a)
+        gs.append(b)
+        ss.append(c)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    step_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    f_s = torch.tensor([float(np.mean(fs))], device="cuda")
+    s_s = torch.tensor([float(np.mean(ss))], device="cuda")
+    for t in (step_ms, f_s, s_s):
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    clocks = sampler.stop() if sampler else None
+    launches = launch_count() - l0
+    if rank == 0:
+        fl = qr_flops(m, n)
+        value = fl / float(f_s) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(step_ms), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Siddon fan-beam A, seeded phantoms, 1% noise)",
+            "config": {"workload": f"config{args.config}: QR of A {m}x{n} + solve {S} slices",
+                       "parallelism": f"1D block-cyclic panels nb={nb} over {world} GPUs, "
+                                      f"NCCL panel broadcast; slices split for the solve"},
+            "pct_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
+            "slices_per_s": S / float(s_s),
+            "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,
+            "factor_ms": float(f_s) * 1e3, "gather_ms": float(np.mean(gs)) * 1e3,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

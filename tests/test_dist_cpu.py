@@ -1,0 +1,121 @@
+"""The multi-GPU schedule (1D block-cyclic panels, one broadcast per panel,
+slice-split solve) run as 2 and 3 CPU processes over gloo with numpy local
+arithmetic; the result must equal the single-process oracle factorization."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import tiled_qr as orc
+from paper_1907_01891_b200 import dist as qd
+
+
+def unit_lower(p):
+    v = np.tril(p, -1)
+    d = min(p.shape)
+    v[np.arange(d), np.arange(d)] = 1.0
+    return v
+
+
+def strided(t, off, rows, cols, ld):
+    flat = t.numpy().reshape(-1)
+    return np.lib.stride_tricks.as_strided(flat[off:], shape=(rows, cols), strides=(8, ld * 8))
+
+
+class NumpyOps:
+    """Test-only local arithmetic: the oracle's Householder sweep (kernels.py:80-101)
+    and T recurrence (kernels.py:134-147) on an m x w panel."""
+
+    def panel(self, a, lda, row0, col0, m, w, tau, t, ldt):
+        p = strided(a, row0 + col0 * lda, m, w, lda)
+        taus = orc._factor_columns(lambda c: (p[c], p[c + 1:]), 0, w)
+        v = unit_lower(p)
+        tf = orc._t_factor(lambda k: v[:, :k].T @ v[:, k], taus)
+        tau.numpy()[:w] = taus
+        strided(t, 0, w, w, ldt)[:, :] = tf
+
+    def apply_qt(self, v, ldv, v_off, m, w, t, ldt, c, ldc, c_off, nc):
+        if nc <= 0:
+            return
+        vu = unit_lower(strided(v, v_off, m, w, ldv).copy())
+        tf = strided(t, 0, w, w, ldt).copy()
+        cm = strided(c, c_off, m, nc, ldc)
+        cm -= vu @ (tf.T @ (vu.T @ cm))
+
+    def sync(self):
+        pass
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def worker(rank, world, port, m, n, nb, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((m, n))
+    lda = m + (m & 1)
+    full = torch.zeros((n, lda), dtype=torch.float64)
+    full[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T))
+    a_local = qd.scatter_block_cyclic(full, n, nb, rank, world)
+    assert a_local.shape[0] == qd.local_cols(n, nb, rank, world)
+    f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, NumpyOps())
+    fact = qd.gather_factored(f)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "factored.npy"), fact[:, :m].numpy().T)
+        np.save(os.path.join(out_dir, "t_all.npy"), f.t_all.numpy())
+    # slice-split solve: every rank solves its share against the gathered factors
+    bmat = rng.standard_normal((m, 7))
+    first, cnt = qd.slice_share(7, rank, world)
+    fm = fact[:, :m].numpy().T.copy()
+    c = bmat[:, first:first + cnt].copy()
+    for k in range(-(-n // nb)):
+        j0, pw = k * nb, min(nb, n - k * nb)
+        vu = unit_lower(fm[j0:, j0:j0 + pw])
+        tf = f.t_all.numpy()[k * nb:k * nb + pw, :pw].T
+        c[j0:] -= vu @ (tf.T @ (vu.T @ c[j0:]))
+    x = np.linalg.solve(np.triu(fm[:n, :n]), c[:n])
+    np.save(os.path.join(out_dir, f"x_{rank}.npy"), x)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,n,nb", [(2, 300, 200, 32), (3, 257, 250, 16), (2, 64, 40, 16)])
+def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb):
+    mp.spawn(worker, args=(world, free_port(), m, n, nb, str(tmp_path)), nprocs=world, join=True)
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((m, n))
+    fact = np.load(tmp_path / "factored.npy")
+    f = orc.factorize_dense(a, 64, 32)
+    r_ref = f.r()
+    r = np.triu(fact[:n])
+    s = np.sign(np.diag(r)) * np.sign(np.diag(r_ref))
+    assert np.abs(r * s[:, None] - r_ref).max() <= 1e-10 * np.abs(r_ref).max()
+    bmat = rng.standard_normal((m, 7))
+    x_ref = orc.solve_dense(f, bmat)
+    parts = []
+    for r_ in range(world):
+        first, cnt = qd.slice_share(7, r_, world)
+        parts.append(np.load(tmp_path / f"x_{r_}.npy"))
+        assert parts[-1].shape == (n, cnt)
+    x = np.concatenate(parts, axis=1)
+    assert np.abs(x - x_ref).max() <= 1e-8 * np.abs(x_ref).max()
+
+
+def test_ownership_helpers():
+    assert qd.local_panels(10, 1, 4) == [1, 5, 9]
+    assert qd.first_local_after(5, 1, 4) == 2   # panels 1, 5 done -> next local is 9
+    assert qd.first_local_after(0, 3, 4) == 0
+    assert sum(qd.local_cols(1000, 128, r, 3) for r in range(3)) == 1000
+    shares = [qd.slice_share(4096, r, 8) for r in range(8)]
+    assert shares[0] == (0, 512) and sum(c for _, c in shares) == 4096
