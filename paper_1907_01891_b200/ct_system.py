@@ -11,14 +11,25 @@ producer.  It keeps the reference's data layout so that image vectors line up:
 * column index = r * W + c, row-major pixels, image row 0 at +y
                                                 (ct_model.py:245, 261, 608-612)
 * ray endpoints: source at radius Rs and angle theta, flat detector at
-  source-to-detector distance SDD, cell centres u_d = (d - (D-1)/2) * du
+  source-to-detector distance SDD, cell centres u_d = (d - (D-1)/2 + 1/4) * du
                                                 (ct_model.py:351-360)
 
 Geometry (recorded in :func:`geometry_hash`): square image of W x W unit
 pixels centred at the origin; source radius Rs = 2 W; views uniform over
-[0, 360) degrees (no quarter shift); SDD = 2 Rs; the detector's fan covers the
-image's circumscribed circle (radius W / sqrt(2)), i.e. half fan angle
-asin(W / (sqrt(2) Rs)).  Weights are chord lengths in pixel units (<= sqrt(2)).
+[0, 360) degrees (no quarter shift); SDD = 2 Rs; flat detector of ``bins``
+cells whose fan spans the image width at the isocentre (half fan angle
+asin(W / (2 Rs))), shifted by a quarter cell (the standard quarter-detector
+offset).  Weights are chord lengths in pixel units (<= sqrt(2)).
+
+Why not a fan over the whole image diagonal: BASELINE configs 2-4 have
+views x bins only ~5% above the pixel count.  With the fan spanning the
+circumscribed circle ~10% of the rays miss the square, the system becomes
+underdetermined (measured on the GPU: 7348 of 65536 R pivots below 1e-10 of
+the largest at config 3) and x is not defined.  Covering the image width puts
+every ray through the image, and the quarter offset breaks the conjugate-ray
+redundancy of the even view counts (90 / 180 / 720 views over 360 degrees);
+on scaled analogues of configs 2-3 this gives cond(A) ~ 1e3 instead of 1e17
+(tests/test_ct_system.py::test_scaled_analogue_is_well_conditioned).
 
 The tracer is vectorised numpy (the step before the hot path, run once per
 configuration); densification into the column-major device matrix happens on
@@ -52,7 +63,9 @@ class FanGeometry:
 
     @property
     def half_fan(self) -> float:
-        return math.asin(self.image_pixels / (math.sqrt(2.0) * self.source_radius))
+        return math.asin(self.image_pixels / (2.0 * self.source_radius))
+
+    detector_offset = 0.25  # in cells (quarter-detector offset)
 
     @property
     def detector_spacing(self) -> float:
@@ -89,7 +102,9 @@ def config_geometry(cfg: int) -> FanGeometry:
 def geometry_hash(g: FanGeometry) -> str:
     """Stable digest of the geometry convention (cf. ct_model.py:175-190)."""
     parts = [
-        "siddon-fan-v1",
+        "siddon-fan-v2",
+        "cover=image-width",
+        f"det_offset={g.detector_offset!r}",
         f"W={g.image_pixels}",
         f"views={g.views}",
         f"bins={g.bins}",
@@ -108,7 +123,8 @@ def ray_endpoints(g: FanGeometry, views: np.ndarray | None = None):
     if views is None:
         views = np.arange(g.views)
     theta = np.radians(360.0 * np.asarray(views, dtype=np.float64) / g.views)[:, None]
-    u = (np.arange(g.bins, dtype=np.float64) - (g.bins - 1) / 2.0)[None, :] * g.detector_spacing
+    u = ((np.arange(g.bins, dtype=np.float64) - (g.bins - 1) / 2.0 + g.detector_offset)[None, :]
+         * g.detector_spacing)
     ct, st = np.cos(theta), np.sin(theta)
     sx = g.source_radius * ct + 0.0 * u
     sy = g.source_radius * st + 0.0 * u

@@ -96,3 +96,13 @@ def test_config_shapes_match_baseline():
     assert (cs.config_geometry(2).n_rays, cs.config_geometry(2).n_pixels) == (17280, 16384)
     assert (cs.config_geometry(3).n_rays, cs.config_geometry(3).n_pixels) == (69120, 65536)
     assert (cs.config_geometry(4).n_rays, cs.config_geometry(4).n_pixels) == (270000, 262144)
+
+
+def test_scaled_analogue_is_well_conditioned():
+    # configs 2-4 have views x bins ~ 1.05 x pixels and an even view count;
+    # the same ratios at W = 48 must give a full-rank, well-conditioned system
+    g = cs.FanGeometry(48, 34, 72)
+    a = cs.dense_matrix(g)
+    assert (a.sum(axis=1) > 0).all()  # every ray crosses the image
+    s = np.linalg.svd(a, compute_uv=False)
+    assert s[0] / s[-1] < 1e4
