@@ -110,6 +110,11 @@ QRB_API int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const dou
 QRB_API int qrb_get_matrix(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
                    int dst_on_device);
 
+/* Enqueue the handle's work on `stream` (cudaStream_t as void*; NULL restores the
+ * handle's own stream, a blocking stream ordered with the legacy default stream).
+ * Use it to order device-pointer calls with a caller's non-default stream. */
+QRB_API int qrb_set_stream(qrb_handle* h, void* stream);
+
 /* Enable (1) / disable (0) per-kernel CUDA-event accounting in qrb_report.kernels. */
 QRB_API int qrb_set_profiling(qrb_handle* h, int on);
 

@@ -323,7 +323,8 @@ struct qrb_handle {
   double* Rinv = nullptr;  // npanels blocks of nb x nb
   bool factored = false;
   bool rinv_ready = false;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream all work of the handle is enqueued on
+  cudaStream_t own_stream = nullptr;  // the handle's own stream
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   DevBuf Bw;  // solve work buffer
   DevBuf resid;
@@ -441,7 +442,10 @@ int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
   if (cudaMalloc(&h->Rinv, sizeof(double) * nb * nb * h->npanels) != cudaSuccess)
     return fail("Rinv alloc");
   cudaGetLastError();
-  QRB_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  // a blocking stream: it orders implicitly with the legacy default stream,
+  // so device buffers produced there (e.g. by torch) are complete before use
+  QRB_CUDA_TRY(cudaStreamCreate(&h->own_stream));
+  h->stream = h->own_stream;
   QRB_CUDA_TRY(cudaEventCreate(&h->ev0));
   QRB_CUDA_TRY(cudaEventCreate(&h->ev1));
   QRB_CUDA_TRY(cudaEventCreate(&h->ev2));
@@ -456,6 +460,7 @@ int qrb_destroy(qrb_handle* h) {
   if (!h) return QRB_OK;
   DeviceGuard g(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->own_stream && h->own_stream != h->stream) cudaStreamSynchronize(h->own_stream);
   if (h->A) cudaFree(h->A);
   if (h->tau) cudaFree(h->tau);
   if (h->T) cudaFree(h->T);
@@ -465,8 +470,16 @@ int qrb_destroy(qrb_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev2) cudaEventDestroy(h->ev2);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
+  return QRB_OK;
+}
+
+int qrb_set_stream(qrb_handle* h, void* stream) {
+  if (!h) return QRB_EARG;
+  DeviceGuard g(h->device);
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
   return QRB_OK;
 }
 

@@ -101,6 +101,13 @@ class QrDevice:
         _native.check(self.lib.qrb_set_matrix(self._h, col0, a.shape[1], _ptr(a), ld, 0),
                       "qrb_set_matrix")
 
+    def set_stream(self, stream_handle: int | None) -> None:
+        """Enqueue this handle's work on a CUDA stream (int handle, e.g.
+        ``torch.cuda.current_stream().cuda_stream``); None = the handle's own
+        blocking stream (ordered with the legacy default stream)."""
+        _native.check(self.lib.qrb_set_stream(self._h, ctypes.c_void_p(stream_handle or 0)),
+                      "qrb_set_stream")
+
     def set_profiling(self, on: bool = True) -> None:
         _native.check(self.lib.qrb_set_profiling(self._h, int(bool(on))), "qrb_set_profiling")
 
