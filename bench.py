@@ -263,6 +263,27 @@ def ours_arm(args, rank: int, world: int):
     resid_dbg = {"explicit": r_explicit[:3].tolist(), "identity": r_dev[:3].tolist(),
                  "x_absmax": float(x_last.abs().max())}
 
+    # config 5: solve throughput of a 4096-slice batch against the config-3 factors
+    cfg5 = None
+    if args.config == 3 and args.cfg5_slices > 0:
+        S5 = args.cfg5_slices
+        x5 = cs.phantom_stack_device(5, S5)                                   # (S5, n)
+        ax5 = (x5 @ a_dev[:, :m]).cpu().numpy().T                             # (m, S5)
+        del x5
+        b5 = torch.zeros((S5, ldb), dtype=torch.float64, device="cuda")
+        b5[:, :m] = torch.from_numpy(np.ascontiguousarray(cs.noisy_sinograms(ax5, 5).T)).cuda()
+        del ax5
+        x5o = torch.zeros((S5, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+        r5 = torch.zeros(S5, dtype=torch.float64, device="cuda")
+        q.solve_device(b5, x5o, r5)                                           # warm-up
+        reps5 = [q.solve_device(b5, x5o, r5) for _ in range(2)]
+        s5_ms = float(np.mean([r["total_ms"] for r in reps5]))
+        cfg5 = {"workload": f"config5: solve {S5} slices on the config-3 factors",
+                "slices": S5, "solve_ms": s5_ms, "slices_per_s": S5 / (s5_ms * 1e-3),
+                "solve_tflops": solve_flops(m, n, S5) / (s5_ms * 1e-3) / 1e12}
+        del b5, x5o, r5
+        torch.cuda.empty_cache()
+
     # end-to-end through the public host API (pinned host A and B, host X out)
     a_pin = torch.empty((n, lda), dtype=torch.float64, pin_memory=True)
     a_pin.copy_(a_dev)
@@ -318,6 +339,7 @@ def ours_arm(args, rank: int, world: int):
                          "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
                                    f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "config5": cfg5,
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s,
     }
@@ -333,6 +355,8 @@ def main():
     ap.add_argument("--slices", type=int, default=None)
     ap.add_argument("--nb", type=int, default=128)
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cfg5-slices", type=int, default=4096,
+                    help="slices of the config-5 solve-throughput run (0 = skip)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")

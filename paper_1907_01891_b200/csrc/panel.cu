@@ -46,6 +46,14 @@ struct PanelArgs {
   unsigned long long* trace;  // optional per-phase timing (QRB_PANEL_TRACE)
 };
 
+// loads of data published by other CTAs before the last grid barrier; the
+// barrier's acquire already invalidated L1, so plain loads are coherent here
+#ifdef QRB_PANEL_LDCG
+#define PART_LD(p) __ldcg(p)
+#else
+#define PART_LD(p) (*(p))
+#endif
+
 __device__ __forceinline__ unsigned long long gtimer() {
   return clock64();
 }
@@ -154,11 +162,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
       if (warp == 0) {
         const double* src = part + (size_t)j * P;
         double t = 0.0;
-        for (int b = lane; b < P; b += 32) t += __ldcg(src + b);
+        for (int b = lane; b < P; b += 32) t += PART_LD(src + b);
         t = warp_sum(t);
         if (lane == 0) {
           scal[0] = t;
-          scal[1] = __ldcg(prow + j);
+          scal[1] = PART_LD(prow + j);
         }
       }
       double v[OWN][MAXB];
@@ -171,9 +179,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
 #pragma unroll
         for (int k = 0; k < MAXB; ++k) {
           const int b = lane + 32 * k;
-          v[i][k] = (need && b < P) ? __ldcg(src + b) : 0.0;
+          v[i][k] = (need && b < P) ? PART_LD(src + b) : 0.0;
         }
-        rv[i] = (need && lane == i) ? __ldcg(prow + c) : 0.0;
+        rv[i] = (need && lane == i) ? PART_LD(prow + c) : 0.0;
       }
       double sm[OWN];
 #pragma unroll
@@ -376,6 +384,11 @@ PanelPlan panel_plan(int m, int w_max) {
   const size_t budget = 200 * 1024;
   int ib = 128;
   while (ib > 8 && panel_smem_bytes(R, ib) > budget) ib >>= 1;
+  static int ib_cap = [] {
+    const char* e = std::getenv("QRB_PANEL_IB");
+    return e ? std::atoi(e) : 128;
+  }();
+  if (ib > ib_cap) ib = ib_cap;
   if (ib > w_max) ib = w_max;
   pl.P = P;
   pl.R = R;

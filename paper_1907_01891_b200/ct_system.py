@@ -244,6 +244,31 @@ def phantom_stack(cfg: int, slices: int, first: int = 0) -> np.ndarray:
     return np.column_stack([rasterize(random_ellipses(r, W), W) for r in rngs])
 
 
+def phantom_stack_device(cfg: int, slices: int, first: int = 0, device="cuda"):
+    """Same phantoms as :func:`phantom_stack` (same per-slice RNG draws),
+    rasterised on the GPU with torch: a (slices, W*W) tensor.  Used for the
+    4096-slice solve-throughput workload (config 5)."""
+    import torch
+
+    W = CONFIGS[cfg]["image"]
+    ell = np.stack([random_ellipses(r, W) for r in slice_rngs(cfg, slices, first)])  # (S,10,6)
+    e = torch.from_numpy(ell).to(device)
+    half = W / 2.0
+    xs = torch.arange(W, dtype=torch.float64, device=device) + 0.5 - half
+    ys = half - (torch.arange(W, dtype=torch.float64, device=device) + 0.5)
+    gy, gx = torch.meshgrid(ys, xs, indexing="ij")
+    gx, gy = gx.reshape(1, -1), gy.reshape(1, -1)
+    img = torch.zeros((slices, W * W), dtype=torch.float64, device=device)
+    for i in range(e.shape[1]):
+        cx, cy, a, b, th, d = (e[:, i, k:k + 1] for k in range(6))
+        t = torch.deg2rad(th)
+        dx, dy = gx - cx, gy - cy
+        u = torch.cos(t) * dx + torch.sin(t) * dy
+        w = -torch.sin(t) * dx + torch.cos(t) * dy
+        img += torch.where((u / a) ** 2 + (w / b) ** 2 <= 1.0, d, torch.zeros_like(d))
+    return img
+
+
 def noisy_sinograms(a_times_x: np.ndarray, cfg: int, first: int = 0) -> np.ndarray:
     """b = A x + eps, eps ~ N(0, (0.01 * max(A x))^2) per slice (seeded)."""
     ax = np.asarray(a_times_x, dtype=np.float64)

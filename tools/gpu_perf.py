@@ -16,6 +16,19 @@ def timeit(fn, reps=3):
         best = min(best, a.elapsed_time(b))
     return best
 
+PANEL_ONLY = "--panel-only" in sys.argv
+if PANEL_ONLY:
+    m = int(sys.argv[-1]); w = 128
+    A = torch.randn(w, m, dtype=torch.float64, device="cuda")
+    tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+    T = torch.zeros(w, w, dtype=torch.float64, device="cuda")
+    A0 = A.clone()
+    def f():
+        A.copy_(A0)
+        lib.qrb_op_panel(P(A), m, m, w, P(tau), P(T), w, None)
+    print(f"panel {m}x{w}: {timeit(f):.3f} ms", flush=True)
+    sys.exit(0)
+
 for (M, N) in [(17280, 16256), (69120, 16384), (69120, 65408)]:
     K = 128
     ld = M
