@@ -173,6 +173,17 @@ QRB_API int qrb_op_gemm_tn(const double* A, int64_t lda, const double* B, int64_
 QRB_API int qrb_op_trsm_upper(const double* R, int64_t ldr, int64_t n, int nb, double* B, int64_t ldb,
                       int64_t nrhs, void* stream);
 
+/* GPU Siddon densifier (the producer of A; reference analogue: Joseph
+ * assemble_system_matrix, ct_model.py:515-547).  `ends` = device array of
+ * 4 x n_rays doubles (sx[], sy[], px[], py[]) for global rows [row0, row0+n_rays);
+ * writes exact intersection lengths (pixel units) of a W x W image (column
+ * index r*W + c, row 0 at +y) into the zeroed column-major A.  Columns are
+ * distributed 1D block-cyclically by panels of nb over `world` ranks; this rank
+ * holds n_local of them (world = 1: A holds all W*W columns).  Stream-ordered. */
+QRB_API int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0, int image_pixels,
+                               double* A, int64_t lda, int nb, int world, int rank,
+                               int64_t n_local, void* stream);
+
 /* Kernels launched by this library since load (gpu_launches accounting). */
 QRB_API int64_t qrb_launch_count(void);
 

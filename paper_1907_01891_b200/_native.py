@@ -89,6 +89,8 @@ SIGNATURES = {
                                c_i64, c_int, c_int, c_int, c_void_p]),
     "qrb_op_trsm_upper": (c_int, [c_void_p, c_i64, c_i64, c_int, c_void_p, c_i64, c_i64,
                                   c_void_p]),
+    "qrb_siddon_densify": (c_int, [c_void_p, c_i64, c_i64, c_int, c_void_p, c_i64, c_int, c_int,
+                                   c_int, c_i64, c_void_p]),
     "qrb_launch_count": (c_i64, []),
     "qrb_release_workspace": (c_int, []),
 }

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "panel.h"
+#include "siddon.h"
 
 #include "../../include/qrb200.h"
 
@@ -806,6 +807,19 @@ int qrb_op_trsm_upper(const double* R, int64_t ldr, int64_t n, int nb, double* B
   MatView Rv{const_cast<double*>(R), n, n, ldr};
   MatView Bv{B, n, nrhs, ldb};
   return trsm_upper(Rv, ws.Wparts.d(), nb, Bv, st);
+}
+
+int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0, int image_pixels,
+                       double* A, int64_t lda, int nb, int world, int rank, int64_t n_local,
+                       void* stream) {
+  if (!ends || !A || n_rays < 0 || image_pixels < 1 || lda < 1 || world < 1 || rank < 0 ||
+      rank >= world || (world > 1 && nb < 1)) {
+    set_last_error("qrb_siddon_densify: bad arguments");
+    return QRB_EARG;
+  }
+  g_launches += 1;
+  return siddon_densify(ends, n_rays, image_pixels, A, lda, row0, nb, world, rank, n_local,
+                        static_cast<cudaStream_t>(stream));
 }
 
 int qrb_release_workspace(void) {

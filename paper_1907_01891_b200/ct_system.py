@@ -189,6 +189,35 @@ def siddon_coo(g: FanGeometry, views_per_block: int = 16):
     return np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
 
 
+def densify_device(g: FanGeometry, lda: int | None = None, rank: int = 0, world: int = 1,
+                   nb: int = 128, views_per_call: int = 64):
+    """Dense column-major A (or this rank's block-cyclic panels) built on the GPU
+    by the sm_100a Siddon kernel (qrb_siddon_densify); returns a torch tensor of
+    shape (local columns, lda).  Bit-identical to :func:`dense_matrix`."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    lib = _native.load()
+    m, n = g.n_rays, g.n_pixels
+    lda = lda or (m + 31) // 32 * 32
+    npan = -(-n // nb)
+    n_local = sum(min(nb, n - k * nb) for k in range(rank, npan, world)) if world > 1 else n
+    a = torch.zeros((n_local, lda), dtype=torch.float64, device="cuda")
+    for v0 in range(0, g.views, views_per_call):
+        views = np.arange(v0, min(g.views, v0 + views_per_call))
+        ends = np.stack([e.ravel() for e in ray_endpoints(g, views)])  # (4, rays)
+        ends_d = torch.from_numpy(np.ascontiguousarray(ends)).cuda()
+        st = lib.qrb_siddon_densify(ctypes.c_void_p(ends_d.data_ptr()), ends.shape[1],
+                                    v0 * g.bins, g.image_pixels, ctypes.c_void_p(a.data_ptr()),
+                                    lda, nb, world, rank, n_local, None)
+        _native.check(st, "qrb_siddon_densify")
+    torch.cuda.synchronize()
+    return a
+
+
 def dense_matrix(g: FanGeometry, order: str = "F") -> np.ndarray:
     """Dense fp64 system matrix on the host (small configurations / tests)."""
     r, c, v = siddon_coo(g)
