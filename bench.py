@@ -115,11 +115,11 @@ class ClockSampler:
 # -- workload ------------------------------------------------------------------------------
 
 
-def build_workload(cfg: int, slices: int | None):
+def build_workload(cfg: int, slices: int | None, host_coo: bool = True):
     from paper_1907_01891_b200 import ct_system as cs
     g = cs.config_geometry(cfg)
     s = slices or cs.CONFIGS[cfg]["slices"]
-    coo = cs.siddon_coo(g)
+    coo = cs.siddon_coo(g) if host_coo else None
     x_true = cs.phantom_stack(cfg, s)
     return g, coo, x_true, s
 
@@ -134,15 +134,18 @@ def densify_device(g, coo, lda: int):
     return a
 
 
-def cpu_sample_tflops(coo, g, steps: int = 1):
+def cpu_sample_tflops(coo, g, steps: int = 1, a_sample=None):
     """Reference algorithm (oracle port, tiled left-looking QR of oocqr) on the
     leading m x 1024 column block of A; returns (TFLOP/s, seconds per run)."""
     from oracle.tiled_qr import factorize_dense
-    r, c, v = coo
     ncol = min(CPU_SAMPLE_COLS, g.n_pixels)
-    sel = c < ncol
-    a = np.zeros((g.n_rays, ncol))
-    a[r[sel], c[sel]] = v[sel]
+    if a_sample is None:
+        r, c, v = coo
+        sel = c < ncol
+        a = np.zeros((g.n_rays, ncol))
+        a[r[sel], c[sel]] = v[sel]
+    else:
+        a = a_sample
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -190,10 +193,13 @@ def ours_arm(args, rank: int, world: int):
 
     torch.cuda.set_device(0)
     t_setup = time.perf_counter()
-    g, coo, x_true, S = build_workload(args.config, args.slices)
+    g, _, x_true, S = build_workload(args.config, args.slices, host_coo=False)
     m, n = g.n_rays, g.n_pixels
     lda = (m + 31) // 32 * 32
-    a_dev = densify_device(g, coo, lda)
+    a_dev = cs.densify_device(g, lda)          # sm_100a Siddon kernel, straight into HBM
+    torch.cuda.synchronize()
+    densify_s = time.perf_counter() - t_setup
+    a_sample = a_dev[:min(CPU_SAMPLE_COLS, n), :m].cpu().numpy().T.copy()
     # sinograms b = A x + 1% noise (seeded per slice); A x via the device matrix
     xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()        # (S, n)
     ax = (xt @ a_dev[:, :m]).cpu().numpy().T                            # (m, S)
@@ -319,7 +325,7 @@ def ours_arm(args, rank: int, world: int):
     q.close()
 
     cores = len(os.sched_getaffinity(0))
-    cpu_val, cpu_t, ncol = cpu_sample_tflops(coo, g)
+    cpu_val, cpu_t, ncol = cpu_sample_tflops(None, g, a_sample=a_sample)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -341,7 +347,7 @@ def ours_arm(args, rank: int, world: int):
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "config5": cfg5,
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
-        "setup_s": setup_s,
+        "setup_s": setup_s, "densify_s": densify_s,
     }
     print(json.dumps(line), flush=True)
 

@@ -208,19 +208,24 @@ def bench_rank(args, rank: int, world: int):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", local_rank))
-    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload,
-                       densify_device, qr_flops, solve_flops)
+    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload, qr_flops,
+                       solve_flops)
     from . import ct_system as cs
     from .device import QrDevice, launch_count
 
-    g, coo, x_true, S = build_workload(args.config, args.slices)
+    g, _, x_true, S = build_workload(args.config, args.slices, host_coo=False)
     m, n, nb = g.n_rays, g.n_pixels, args.nb
     lda = (m + 31) // 32 * 32
-    a_full = densify_device(g, coo, lda)
-    xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()
-    b_host = cs.noisy_sinograms((xt @ a_full[:, :m]).cpu().numpy().T, args.config)
-    a_pristine = scatter_block_cyclic(a_full, n, nb, rank, world)
-    del a_full, xt
+    # each rank densifies only its own block-cyclic panels on its GPU
+    a_pristine = cs.densify_device(g, lda, rank=rank, world=world, nb=nb)
+    cols = [c for k in local_panels(-(-n // nb), rank, world)
+            for c in range(k * nb, min(n, (k + 1) * nb))]
+    xt = torch.from_numpy(np.ascontiguousarray(x_true[cols].T)).cuda()
+    ax = xt @ a_pristine[:, :m]                       # this rank's share of A x
+    if world > 1:
+        dist.all_reduce(ax)
+    b_host = cs.noisy_sinograms(ax.cpu().numpy().T, args.config)
+    del xt, ax
     torch.cuda.empty_cache()
     first, cnt = slice_share(S, rank, world)
     b_dev = torch.zeros((max(cnt, 1), lda), dtype=torch.float64, device="cuda")
