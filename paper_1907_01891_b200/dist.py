@@ -99,10 +99,28 @@ class DistFactors:
     stats: dict = field(default_factory=dict)
 
 
+def _panel_views(buf, m: int, n: int, nb: int, k: int):
+    j0 = k * nb
+    pw = min(nb, n - j0)
+    mk = m - j0
+    ldv = mk + (mk & 1)
+    nelem = ldv * pw + nb * nb + nb
+    return (j0, pw, mk, ldv, nelem, buf[: ldv * pw].view(pw, ldv),
+            buf[ldv * pw: ldv * pw + nb * nb].view(nb, nb), buf[ldv * pw + nb * nb: nelem])
+
+
 def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int, world: int,
-                          ops, group=None) -> DistFactors:
+                          ops, group=None, lookahead: bool = True) -> DistFactors:
     """Blocked Householder QR of the block-cyclic matrix; a_local is overwritten
-    with the local panels of the factored matrix (R above, V below)."""
+    with the local panels of the factored matrix (R above, V below).
+
+    With ``lookahead`` (depth 1) the owner of panel k+1 first applies Q_k^T to
+    that panel only, factors it and starts its broadcast, and only then updates
+    the rest of its trailing columns; the other ranks receive panel k+1 while
+    they are still busy with step k.  Each rank factors 1/G of the panels, so
+    the panel latency is spread over the G GPUs instead of serialising every
+    step.  Panels travel in two alternating buffers.
+    """
     import torch
     import torch.distributed as dist
 
@@ -112,38 +130,66 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
     t_all = torch.zeros((npan * nb, nb), dtype=dt, device=dev)
     tau_all = torch.zeros(npan * nb, dtype=dt, device=dev)
     ldv_max = m + (m & 1)
-    buf = torch.empty(ldv_max * nb + nb * nb + nb, dtype=dt, device=dev)
+    bufs = [torch.empty(ldv_max * nb + nb * nb + nb, dtype=dt, device=dev) for _ in range(2)]
     n_local = a_local.shape[0]
-    bytes_bcast = 0
+    stats = {"bytes_broadcast": 0, "panels": npan, "lookahead": bool(lookahead and world > 1)}
+
+    def factor_and_pack(k):
+        j0, pw, mk, ldv, nelem, vview, tview, tauv = _panel_views(bufs[k % 2], m, n, nb, k)
+        lcol = (k // world) * nb
+        tview.zero_()
+        ops.panel(a_local, lda, j0, lcol, mk, pw, tauv, tview, nb)
+        vview[:, :mk].copy_(a_local[lcol:lcol + pw, j0:m])
+
+    def start_bcast(k):
+        nelem = _panel_views(bufs[k % 2], m, n, nb, k)[4]
+        if world == 1:
+            return None
+        stats["bytes_broadcast"] += 8 * nelem
+        return dist.broadcast(bufs[k % 2][:nelem], src=owner_of(k, world), group=group,
+                              async_op=True)
+
+    def apply(k, col_from, col_to):
+        if col_to <= col_from:
+            return
+        j0, pw, mk, ldv, _, vview, tview, _ = _panel_views(bufs[k % 2], m, n, nb, k)
+        ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, a_local, lda, j0 + col_from * lda,
+                     col_to - col_from)
+
+    la = lookahead and world > 1
     ops.sync()
     t0 = time.perf_counter()
+    if rank == owner_of(0, world):
+        factor_and_pack(0)
+    pending = start_bcast(0)
     for k in range(npan):
-        j0 = k * nb
-        pw = min(nb, n - j0)
-        mk = m - j0
-        ldv = mk + (mk & 1)
-        root = owner_of(k, world)
-        nelem = ldv * pw + nb * nb + nb
-        vview = buf[: ldv * pw].view(pw, ldv)
-        tview = buf[ldv * pw: ldv * pw + nb * nb].view(nb, nb)
-        tauv = buf[ldv * pw + nb * nb: nelem]
-        if rank == root:
-            lcol = (k // world) * nb
-            tview.zero_()
-            ops.panel(a_local, lda, j0, lcol, mk, pw, tauv, tview, nb)
-            vview[:, :mk].copy_(a_local[lcol:lcol + pw, j0:m])
-        if world > 1:
-            dist.broadcast(buf[:nelem], src=root, group=group)
-            bytes_bcast += 8 * nelem
+        if pending is not None:
+            pending.wait()
+        j0, pw, mk, ldv, _, vview, tview, tauv = _panel_views(bufs[k % 2], m, n, nb, k)
         t_all[k * nb:(k + 1) * nb].copy_(tview)
         tau_all[j0:j0 + pw].copy_(tauv[:pw])
         lfirst = first_local_after(k, rank, world) * nb
-        ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, a_local, lda, j0 + lfirst * lda,
-                     n_local - lfirst)
+        nxt = k + 1
+        pending = None
+        if nxt < npan and rank == owner_of(nxt, world):
+            # panel k+1 is this rank's local panel starting at lfirst
+            pw1 = min(nb, n - nxt * nb)
+            apply(k, lfirst, lfirst + pw1)
+            factor_and_pack(nxt)
+            if la:
+                pending = start_bcast(nxt)
+            apply(k, lfirst + pw1, n_local)
+            if not la:
+                pending = start_bcast(nxt)
+        else:
+            if la and nxt < npan:
+                pending = start_bcast(nxt)   # receive while updating
+            apply(k, lfirst, n_local)
+            if not la and nxt < npan:
+                pending = start_bcast(nxt)
     ops.sync()
     secs = time.perf_counter() - t0
-    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs,
-                       {"bytes_broadcast": bytes_bcast, "panels": npan})
+    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats)
 
 
 def gather_factored(f: DistFactors, group=None, place=None):

@@ -59,7 +59,7 @@ def free_port():
     return port
 
 
-def worker(rank, world, port, m, n, nb, out_dir):
+def worker(rank, world, port, m, n, nb, out_dir, lookahead=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(7)
@@ -69,7 +69,8 @@ def worker(rank, world, port, m, n, nb, out_dir):
     full[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T))
     a_local = qd.scatter_block_cyclic(full, n, nb, rank, world)
     assert a_local.shape[0] == qd.local_cols(n, nb, rank, world)
-    f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, NumpyOps())
+    f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, NumpyOps(),
+                                 lookahead=lookahead)
     fact = qd.gather_factored(f)
     if rank == 0:
         np.save(os.path.join(out_dir, "factored.npy"), fact[:, :m].numpy().T)
@@ -90,9 +91,12 @@ def worker(rank, world, port, m, n, nb, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,n,nb", [(2, 300, 200, 32), (3, 257, 250, 16), (2, 64, 40, 16)])
-def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb):
-    mp.spawn(worker, args=(world, free_port(), m, n, nb, str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,m,n,nb,la", [(2, 300, 200, 32, True), (3, 257, 250, 16, True),
+                                             (2, 64, 40, 16, True), (2, 300, 200, 32, False),
+                                             (4, 200, 150, 16, True)])
+def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb, la):
+    mp.spawn(worker, args=(world, free_port(), m, n, nb, str(tmp_path), la), nprocs=world,
+             join=True)
     rng = np.random.default_rng(7)
     a = rng.standard_normal((m, n))
     fact = np.load(tmp_path / "factored.npy")
