@@ -184,6 +184,13 @@ QRB_API int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0,
                                double* A, int64_t lda, int nb, int world, int rank,
                                int64_t n_local, void* stream);
 
+/* Stream-ordered strided copy of a rows x cols column-major block (pitched);
+ * kind: 0 = host->device, 1 = device->host, 2 = device->device, 3 = host->host.
+ * The host-staged (out-of-HBM) path streams reflector panels with it
+ * (reference analogue: TileCache staging, tile_store.py:225-415). */
+QRB_API int qrb_copy_2d(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                        int64_t cols, int kind, void* stream);
+
 /* Kernels launched by this library since load (gpu_launches accounting). */
 QRB_API int64_t qrb_launch_count(void);
 

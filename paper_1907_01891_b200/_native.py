@@ -91,6 +91,7 @@ SIGNATURES = {
                                   c_void_p]),
     "qrb_siddon_densify": (c_int, [c_void_p, c_i64, c_i64, c_int, c_void_p, c_i64, c_int, c_int,
                                    c_int, c_i64, c_void_p]),
+    "qrb_copy_2d": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_i64, c_i64, c_int, c_void_p]),
     "qrb_launch_count": (c_i64, []),
     "qrb_release_workspace": (c_int, []),
 }

@@ -822,6 +822,21 @@ int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0, int ima
                         static_cast<cudaStream_t>(stream));
 }
 
+int qrb_copy_2d(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                int64_t cols, int kind, void* stream) {
+  if (!dst || !src || rows < 0 || cols < 0 || ldd < rows || lds < rows || kind < 0 || kind > 3) {
+    set_last_error("qrb_copy_2d: bad arguments");
+    return QRB_EARG;
+  }
+  if (rows == 0 || cols == 0) return QRB_OK;
+  static const cudaMemcpyKind kinds[4] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                          cudaMemcpyDeviceToDevice, cudaMemcpyHostToHost};
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
+                                 rows * sizeof(double), cols, kinds[kind],
+                                 static_cast<cudaStream_t>(stream)));
+  return QRB_OK;
+}
+
 int qrb_release_workspace(void) {
   cudaDeviceSynchronize();
   device_workspace().release();
