@@ -74,6 +74,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // entry V[:, c]^T v_j of the T recurrence for c < j (kernels.py:143-146).
 // Partial buffers alternate by column parity, so a CTA that races ahead into
 // column j+1 never overwrites partials another CTA is still summing.
+template <int OWN>  // columns owned per warp: ceil(ib / 16)
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p) {
   extern __shared__ double smem_d[];
   const int R = p.R;
@@ -103,7 +104,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
   // column c is owned by warp c % PANEL_WARPS: that warp computes its partial
   // sums, reduces its w_c after the barrier and applies its rank-1 update, so
   // the only intra-CTA synchronisation per column is one __syncthreads.
-  constexpr int OWN = 8;  // columns per warp (ib <= 128)
   constexpr int MAXB = 5;  // partial loads per lane (P <= 160)
   for (int j = 0; j < ib; ++j) {
     unsigned long long ta = tracing ? gtimer() : 0, tb = 0;
@@ -270,33 +270,63 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
 }
 
 // T from the Gram matrix: T[k,k] = tau_k, T[:k,k] = -tau_k * T[:k,:k] G[:k,k]
+// (kernels.py:134-147).  Blocked by 32: the diagonal 32 x 32 blocks follow the
+// column recurrence inside one warp each (warp-synchronous, no block barriers),
+// then the off-diagonal blocks are filled block column by block column with
+// T[I,J] = -T[I,I..J-1] G[I..J-1, J] T[J,J]-style products that need only one
+// __syncthreads per block column:  for the block column J,
+//   Z = G[0:j0, J] T[J,J]     (j0 x 32)
+//   T[0:j0, J] = -T[0:j0, 0:j0] Z
+// which is the recurrence applied 32 columns at a time.
 constexpr int BT_THREADS = 512;
 __global__ void __launch_bounds__(BT_THREADS) build_t_kernel(const double* G, int ldg,
                                                              const double* tau, int w, double* T,
                                                              int ldt) {
-  extern __shared__ double ts[];  // w*w column-major + w (g column)
-  double* gcol = ts + (size_t)w * w;
-  for (int i = threadIdx.x; i < w * w; i += BT_THREADS) ts[i] = 0.0;
-  const int sub_n = BT_THREADS / w >= 4 ? 4 : (BT_THREADS / w >= 2 ? 2 : 1);
+  extern __shared__ double ts[];  // T: w*w column-major, then Z: w*32
+  double* z = ts + (size_t)w * w;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < w * w; i += BT_THREADS) ts[i] = 0.0;
   __syncthreads();
-  for (int j = 0; j < w; ++j) {
-    const double tj = tau[j];
-    for (int i = threadIdx.x; i < j; i += BT_THREADS) gcol[i] = G[i + (int64_t)j * ldg];
-    __syncthreads();
-    if (tj != 0.0 && j > 0) {
-      // rows i < j, sub_n threads per row (consecutive lanes)
-      const int i = threadIdx.x / sub_n;
-      const int sub = threadIdx.x % sub_n;
-      double s = 0.0;
-      if (i < j)
-        for (int l = i + sub; l < j; l += sub_n) s += ts[i + (size_t)l * w] * gcol[l];
-      for (int o = sub_n / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, sub_n);
-      if (i < j && sub == 0) ts[i + (size_t)j * w] = -tj * s;
+  // strict upper Gram entries, read through the read-only path (tiny, cached)
+  auto gs_at = [&](int r, int c) { return __ldg(G + r + (int64_t)c * ldg); };
+  const int nblk = (w + 31) / 32;
+  // diagonal blocks: warp b handles block b with the plain recurrence
+  for (int b = warp; b < nblk; b += BT_THREADS / 32) {
+    const int o = b * 32, bw = min(32, w - o);
+    for (int j = 0; j < bw; ++j) {
+      const double tj = tau[o + j];
+      // lane i < j: s_i = sum_{l=i}^{j-1} T[o+i][o+l] G[o+l][o+j]
+      double sacc = 0.0;
+      if (lane < j)
+        for (int l = lane; l < j; ++l) sacc += ts[(o + lane) + (size_t)(o + l) * w] * gs_at(o + l, o + j);
+      __syncwarp();
+      if (lane < j) ts[(o + lane) + (size_t)(o + j) * w] = (tj != 0.0) ? -tj * sacc : 0.0;
+      if (lane == j) ts[(o + j) + (size_t)(o + j) * w] = tj;
+      __syncwarp();
     }
-    if (threadIdx.x == 0) ts[j + (size_t)j * w] = tj;
+  }
+  __syncthreads();
+  // off-diagonal block columns J = 1..nblk-1
+  for (int J = 1; J < nblk; ++J) {
+    const int j0 = J * 32, bw = min(32, w - j0);
+    // Z[0:j0, 0:bw] = G[0:j0, J] * T[J,J]
+    for (int idx = tid; idx < j0 * bw; idx += BT_THREADS) {
+      const int c = idx / j0, r = idx - c * j0;
+      double sacc = 0.0;
+      for (int l = 0; l <= c; ++l) sacc += gs_at(r, j0 + l) * ts[(j0 + l) + (size_t)(j0 + c) * w];
+      z[r + (size_t)c * w] = sacc;
+    }
+    __syncthreads();
+    // T[0:j0, J] = -T[0:j0, 0:j0] Z
+    for (int idx = tid; idx < j0 * bw; idx += BT_THREADS) {
+      const int c = idx / j0, r = idx - c * j0;
+      double sacc = 0.0;
+      for (int l = r; l < j0; ++l) sacc += ts[r + (size_t)l * w] * z[l + (size_t)c * w];
+      ts[r + (size_t)(j0 + c) * w] = -sacc;
+    }
     __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < w * w; idx += BT_THREADS) {
+  for (int idx = tid; idx < w * w; idx += BT_THREADS) {
     const int c = idx / w, r = idx - c * w;
     T[r + (int64_t)c * ldt] = ts[idx];
   }
@@ -309,9 +339,18 @@ __global__ void reduce_splits_kernel(const double* parts, int64_t split_stride, 
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx / rows, r = idx - c * rows;
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += parts[z * split_stride + r + c * ldp];
-    out[r + c * ldo] = s;
+    const double* src = parts + r + c * ldp;
+    // 4 independent partial chains (loads in flight), combined in fixed order
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {
+      s0 += src[(int64_t)(z + 0) * split_stride];
+      s1 += src[(int64_t)(z + 1) * split_stride];
+      s2 += src[(int64_t)(z + 2) * split_stride];
+      s3 += src[(int64_t)(z + 3) * split_stride];
+    }
+    for (; z < splits; ++z) s0 += src[(int64_t)z * split_stride];
+    out[r + c * ldo] = (s0 + s1) + (s2 + s3);
   }
 }
 
@@ -415,11 +454,22 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
     return QRB_ERR_ARG;
   }
   const size_t smem = panel_smem_bytes(R, ib);
-  static size_t configured = 0;
-  if (smem > configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  void* fn;
+  const int own = (ib + PANEL_WARPS - 1) / PANEL_WARPS;
+  if (own <= 1)
+    fn = reinterpret_cast<void*>(panel_qr_kernel<1>);
+  else if (own <= 2)
+    fn = reinterpret_cast<void*>(panel_qr_kernel<2>);
+  else if (own <= 4)
+    fn = reinterpret_cast<void*>(panel_qr_kernel<4>);
+  else
+    fn = reinterpret_cast<void*>(panel_qr_kernel<8>);
+  static size_t configured[4] = {0, 0, 0, 0};
+  const int slot = own <= 1 ? 0 : own <= 2 ? 1 : own <= 4 ? 2 : 3;
+  if (smem > configured[slot]) {
+    QRB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-    configured = smem;
+    configured[slot] = smem;
   }
   QRB_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned int), stream));
   PanelArgs a;
@@ -444,7 +494,7 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
     a.trace = trace_buf;
   }
   void* args[] = {&a};
-  QRB_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(panel_qr_kernel), dim3(P),
+  QRB_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P),
                                            dim3(PANEL_THREADS), args, smem, stream));
   if (trace_on) {
     static int calls = 0;
@@ -468,7 +518,7 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
 
 int build_t(const double* G, int ldg, const double* tau, int w, double* T, int ldt,
             cudaStream_t stream) {
-  const size_t smem = ((size_t)w * w + w) * sizeof(double);
+  const size_t smem = ((size_t)w * w + (size_t)w * 32) * sizeof(double);
   static size_t configured = 0;
   if (smem > configured) {
     QRB_CUDA_TRY(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -484,8 +534,8 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
                   int64_t ldp, double* out, int64_t ldo, cudaStream_t stream) {
   const int64_t total = (int64_t)rows * cols;
   if (total == 0) return QRB_OK;
-  int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * 148));
-  reduce_splits_kernel<<<blocks, 256, 0, stream>>>(parts, split_stride, splits, rows, cols, ldp,
+  int blocks = static_cast<int>(std::min<int64_t>((total + 127) / 128, 8 * 148));
+  reduce_splits_kernel<<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols, ldp,
                                                    out, ldo);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
