@@ -449,6 +449,134 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// persistent C -= A B with an L2 reduce-add epilogue: the consumers stage -acc
+// column by column in shared memory (padded 1040-byte columns, conflict-free)
+// and 64 threads each issue one cp.reduce.async.bulk .add.f64 of their column
+// into C, which the L2 applies in place.  No C tile is loaded into the SM at
+// all, so the epilogue is a handful of STS per thread plus one barrier.
+// ---------------------------------------------------------------------------
+constexpr int RA_STAGES = 6;
+constexpr int RA_COL_BYTES = BM * 8 + 16;
+constexpr uint32_t RA_STAGING = NN_BN * RA_COL_BYTES;
+constexpr int RA_SMEM = RA_STAGES * NN_STAGE_BYTES + RA_STAGING + 1024 + 256;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_nn_sub_redadd(const __grid_constant__ CUtensorMap mapA,
+                       const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
+                       const int64_t ldc, const NnArgs args) {
+  constexpr int NT = NN_BN / 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stage = smem + RA_STAGES * NN_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + RA_STAGING);
+  uint64_t* empty = full + RA_STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + NN_BN - 1) / NN_BN;
+  const int num_k = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RA_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {
+    if (lane == 0) {
+      prefetch_tmap(&mapA);
+      prefetch_tmap(&mapB);
+      int kit = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+        for (int kt = 0; kt < num_k; ++kt, ++kit) {
+          const int s = kit % RA_STAGES;
+          if (kit >= RA_STAGES) mbar_wait(&empty[s], ((kit / RA_STAGES) & 1) ^ 1);
+          uint8_t* sA = smem + s * NN_STAGE_BYTES;
+          uint8_t* sB = sA + NN_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], NN_STAGE_BYTES);
+          const int k = kt * BK;
+#pragma unroll
+          for (int mb = 0; mb < BM / 16; ++mb)
+            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+          tma_load_2d(sB, &mapB, k, n_tile * NN_BN, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2;
+  const int q = lane & 3;
+  const int m0 = (warp & 3) * 32;
+  const int n0 = (warp >> 2) * (NN_BN / 2);
+  int kit = 0;
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+    int m_tile, n_tile;
+    decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+    const int mg0 = m_tile * BM;
+    const int ng0 = n_tile * NN_BN;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < num_k; ++kt, ++kit) {
+      const int s = kit % RA_STAGES;
+      mbar_wait(&full[s], (kit / RA_STAGES) & 1);
+      const uint8_t* sA = smem + s * NN_STAGE_BYTES;
+      const uint8_t* sB = sA + NN_A_BYTES;
+      const int kg0 = kt * BK;
+      if (args.mask_a && mg0 <= kg0 + BK - 1)
+        consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else
+        consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // the previous tile's bulk reduces must have finished reading the staging
+    // (waited for here, one tile later, so the issuing warps never stall)
+    if (threadIdx.x < NN_BN) bulk_wait_read0();
+    named_bar_sync(1, CONSUMER_WARPS * 32);
+#pragma unroll
+    for (int mp = 0; mp < 2; ++mp) {
+      const int m = m0 + mp * 16 + 2 * g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + nt * 8 + rp(2 * q + e);
+          *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
+              make_double2(-acc[mp * 2 + 0][nt][e], -acc[mp * 2 + 1][nt][e]);
+        }
+      }
+    }
+    fence_proxy_async();
+    named_bar_sync(1, CONSUMER_WARPS * 32);
+    if (threadIdx.x < NN_BN) {
+      const int n = threadIdx.x;
+      const int rows = min(BM, args.M - mg0);
+      if (ng0 + n < args.N && rows > 0) {
+        double* dst = C + mg0 + static_cast<int64_t>(ng0 + n) * ldc;
+        const int even = rows & ~1;
+        if (even) bulk_reduce_add_f64(dst, stage + n * RA_COL_BYTES, even * 8);
+        if (rows & 1)
+          atomicAdd(dst + even,
+                    *reinterpret_cast<const double*>(stage + n * RA_COL_BYTES + even * 8));
+        bulk_commit();
+      }
+    }
+  }
+  if (threadIdx.x < NN_BN) bulk_wait0();
+}
+
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -592,6 +720,31 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   if ((reinterpret_cast<uintptr_t>(out) & 15) != 0 || (ldo & 1) != 0) {
     set_last_error("gemm_nn: output must be 16-byte aligned with even ld");
     return QRB_ERR_ARG;
+  }
+  static const bool redadd = std::getenv("QRB_NN_STAGED_C") == nullptr;
+  if (epi == GEMM_EPI_SUB && redadd && !(std::getenv("QRB_NN_CLASSIC"))) {
+    static bool configured_ra = false;
+    if (!configured_ra) {
+      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_redadd,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, RA_SMEM));
+      configured_ra = true;
+    }
+    CUtensorMap ma, mb;
+    QRB_TRY(make_map(&ma, a_mm, 16, BK));
+    QRB_TRY(make_map(&mb, b, BK, NN_BN));
+    NnArgs args;
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.mask_a = mask_a;
+    args.group_m = 16;
+    const int num_m = (M + BM - 1) / BM;
+    const int num_n = (N + NN_BN - 1) / NN_BN;
+    args.num_tiles = num_m * num_n;
+    const int grid = std::min(args.num_tiles, gemm_sm_count());
+    gemm_nn_sub_redadd<<<grid, THREADS, RA_SMEM, stream>>>(ma, mb, out, ldo, args);
+    QRB_CUDA_TRY(cudaGetLastError());
+    return QRB_OK;
   }
   if (epi == GEMM_EPI_SUB && !(std::getenv("QRB_NN_CLASSIC"))) {
     static bool configured = false;
