@@ -317,6 +317,26 @@ def bench_rank(args, rank: int, world: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     clocks = sampler.stop() if sampler else None
     launches = launch_count() - l0
+
+    # end to end through host buffers: this rank's panels from pinned host memory
+    # in, its slice share of X out (factorization + gather + solve inside)
+    a_pin = torch.empty(a_pristine.shape, dtype=torch.float64, pin_memory=True)
+    a_pin.copy_(a_pristine)
+    b_pin = torch.empty((max(cnt, 1), lda), dtype=torch.float64, pin_memory=True)
+    b_pin.copy_(b_dev)
+    x_pin = torch.empty((max(cnt, 1), n), dtype=torch.float64, pin_memory=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter()
+    a_local.copy_(a_pin, non_blocking=True)
+    f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
+    gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
+    q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+    if cnt:
+        q.solve(b_pin.numpy().T[:m, :cnt], out=x_pin.numpy().T[:, :cnt])
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t_e2e], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     if rank == 0:
         fl = qr_flops(m, n)
         value = fl / float(f_s) / 1e12
@@ -333,7 +353,12 @@ def bench_rank(args, rank: int, world: int):
             "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,
             "factor_ms": float(f_s) * 1e3, "gather_ms": float(np.mean(gs)) * 1e3,
             "gpu_launches": int(launches), "clocks": clocks,
-            "e2e": None,
+            "e2e": {"value": fl / float(e2e_s) / 1e12, "unit": UNIT,
+                    "h2d_bytes_per_step": int(8 * lda * n + 8 * m * S),
+                    "d2h_bytes_per_step": int(8 * n * S),
+                    "ms_per_step": float(e2e_s) * 1e3,
+                    "path": "pinned host panels -> factorize_distributed -> all-gather -> "
+                            "QrDevice.solve(host B share -> host X share); max over ranks"},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
