@@ -30,6 +30,7 @@ namespace qrb {
 namespace {
 
 constexpr int PANEL_THREADS = 512;
+constexpr int PART_REPL = 1;  // >1 tried: no gain (loads are MLP-bound, not line-bound)
 constexpr int PANEL_WARPS = PANEL_THREADS / 32;
 
 struct PanelArgs {
@@ -90,7 +91,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
   const int warp = tid >> 5, lane = tid & 31;
   const int r0 = cta * R;
   const int nrows = max(0, min(R, p.m - r0));
-  const size_t buf_stride = (size_t)(ib + 1) * P + ib + 8;
+  // the partial-sum vectors are written PART_REPL times and each CTA reads the
+  // copy cta % PART_REPL, so every L2 line is hit by P / PART_REPL readers
+  // instead of all P (the all-to-all re-sum is L2 line-contention bound)
+  const size_t repl_stride = (size_t)(ib + 1) * P;
+  const size_t buf_stride = repl_stride * PART_REPL + ib + 8;
   unsigned int nbar = 0;
 
   for (int idx = tid; idx < ib * R; idx += PANEL_THREADS) {
@@ -107,8 +112,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
   constexpr int MAXB = 5;  // partial loads per lane (P <= 160)
   for (int j = 0; j < ib; ++j) {
     unsigned long long ta = tracing ? gtimer() : 0, tb = 0;
-    double* part = p.part + (size_t)(j & 1) * buf_stride;  // [c * P + cta]
-    double* prow = part + (size_t)(ib + 1) * P;             // pivot row j
+    double* part_w = p.part + (size_t)(j & 1) * buf_stride;      // replica 0
+    double* part = part_w + (size_t)(cta % PART_REPL) * repl_stride;  // my read replica
+    double* prow = part_w + repl_stride * PART_REPL;                // pivot row j
     const int lj = j - r0;
     const bool owner = lj >= 0 && lj < nrows;
     double* x = slab + (size_t)j * R;
@@ -137,7 +143,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
         for (int i = 1; i < OWN; ++i)
           if (lane == i) v = acc[i];
         const int c = warp + lane * PANEL_WARPS;
-        if (c < ib) part[(size_t)c * P + cta] = v;  // c == j holds sigma
+        if (c < ib)  // c == j holds sigma
+#pragma unroll
+          for (int r = 0; r < PART_REPL; ++r) part_w[r * repl_stride + (size_t)c * P + cta] = v;
       }
     }
     if (owner)
@@ -414,7 +422,11 @@ int panel_max_ctas() {
 PanelPlan panel_plan(int m, int w_max) {
   PanelPlan pl;
   const int cap = panel_max_ctas();
-  int P = (m + 63) / 64;
+  static int min_rows = [] {
+    const char* e = std::getenv("QRB_PANEL_MINROWS");
+    return e ? std::max(16, std::atoi(e)) : 64;
+  }();
+  int P = (m + min_rows - 1) / min_rows;
   if (P > cap) P = cap;
   if (P < 1) P = 1;
   int R = (m + P - 1) / P;
@@ -425,7 +437,7 @@ PanelPlan panel_plan(int m, int w_max) {
   while (ib > 8 && panel_smem_bytes(R, ib) > budget) ib >>= 1;
   static int ib_cap = [] {
     const char* e = std::getenv("QRB_PANEL_IB");
-    return e ? std::atoi(e) : 128;
+    return e ? std::atoi(e) : 64;  // measured best cap (r01 sweep, m = 2160 .. 69120)
   }();
   if (ib > ib_cap) ib = ib_cap;
   if (ib > w_max) ib = w_max;
@@ -439,7 +451,9 @@ size_t panel_smem_bytes(int R, int ib) {
   return ((size_t)ib * R + 2 * (size_t)ib + 8) * sizeof(double);
 }
 
-size_t panel_part_doubles(int P, int ib) { return 2 * ((size_t)(ib + 1) * P + ib + 8); }
+size_t panel_part_doubles(int P, int ib) {
+  return 2 * ((size_t)(ib + 1) * P * PART_REPL + ib + 8);
+}
 
 int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int ldg,
                  double* part, unsigned int* bar, cudaStream_t stream) {
