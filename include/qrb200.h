@@ -156,6 +156,15 @@ QRB_API int qrb_op_panel(double* panel, int64_t ldp, int64_t m, int64_t w, doubl
 QRB_API int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
                     int64_t ldt, double* C, int64_t ldc, int64_t nc, void* stream);
 
+/* Reference-format interop: [F; G] <- Q^T [F; G] for a triangle-on-dense tile
+ * factorization produced by the reference (D = b x b reflector tile, S = its
+ * packed T tile with inner width w, F / G = b x nc blocks).  Replaces
+ * apply_left_qt_td (kernels.py:385-405) so the GPU can solve against factors
+ * the CPU reference computed (apply_left_qt_dense maps onto qrb_op_apply_qt). */
+QRB_API int qrb_op_apply_qt_td(const double* D, int64_t ldd, int64_t b, int64_t w, const double* S,
+                               int64_t lds, double* F, int64_t ldf, double* G, int64_t ldg,
+                               int64_t nc, void* stream);
+
 /* C <- C - A B (A m x k, B k x n).  Replaces gemm_nn_mo (kernels.py:442-455). */
 QRB_API int qrb_op_gemm_nn_sub(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                        int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "qrb_op_panel": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p, c_i64, c_void_p]),
     "qrb_op_apply_qt": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_void_p, c_i64,
                                 c_i64, c_void_p]),
+    "qrb_op_apply_qt_td": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_void_p,
+                                   c_i64, c_void_p, c_i64, c_i64, c_void_p]),
     "qrb_op_gemm_nn_sub": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_i64, c_i64,
                                    c_i64, c_i64, c_void_p]),
     "qrb_op_gemm_tn": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_i64, c_i64, c_i64,

@@ -406,7 +406,28 @@ __global__ void column_sumsq_kernel(const double* B, int64_t ldb, int r0, int r1
   }
 }
 
+// Y += alpha * X on a rows x cols column-major block
+__global__ void axpy_block_kernel(double alpha, const double* X, int64_t ldx, double* Y,
+                                  int64_t ldy, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / rows, r = idx - c * rows;
+    Y[r + c * ldy] += alpha * X[r + c * ldx];
+  }
+}
+
 }  // namespace
+
+int axpy_block(double alpha, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t rows,
+               int64_t cols, cudaStream_t stream) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return QRB_OK;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * 148));
+  axpy_block_kernel<<<blocks, 256, 0, stream>>>(alpha, X, ldx, Y, ldy, rows, cols);
+  QRB_CUDA_TRY(cudaGetLastError());
+  return QRB_OK;
+}
 
 int panel_max_ctas() {
   static int cap = -1;

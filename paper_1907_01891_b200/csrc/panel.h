@@ -30,6 +30,9 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
 
 int trtri_blocks(const double* A, int64_t lda, int n, int bs, double* Rinv, cudaStream_t stream);
 
+int axpy_block(double alpha, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t rows,
+               int64_t cols, cudaStream_t stream);
+
 int column_sumsq(const double* B, int64_t ldb, int r0, int r1, int ncols, double* out,
                  cudaStream_t stream);
 

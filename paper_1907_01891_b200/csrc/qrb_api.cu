@@ -822,6 +822,41 @@ int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0, int ima
                         static_cast<cudaStream_t>(stream));
 }
 
+int qrb_op_apply_qt_td(const double* D, int64_t ldd, int64_t b, int64_t w, const double* S,
+                       int64_t lds, double* F, int64_t ldf, double* G, int64_t ldg, int64_t nc,
+                       void* stream) {
+  if (!D || !S || !F || !G || b < 1 || w < 1 || w > 128 || nc < 0 || (ldd & 1) || (lds & 1) ||
+      (ldf & 1) || (ldg & 1)) {
+    set_last_error("qrb_op_apply_qt_td: bad arguments (leading dimensions must be even)");
+    return QRB_EARG;
+  }
+  if (nc == 0) return QRB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace& ws = device_workspace();
+  const int64_t ldw = even(w);
+  QRB_TRY(ws.W.ensure(sizeof(double) * ldw * nc, st));
+  QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));
+  // reference apply_left_qt_td (kernels.py:385-405): per inner panel j0 of width pw
+  //   W = F[j0:j0+pw] + Vd^T G ;  Z = S_p^T W ;  F[j0:j0+pw] -= Z ;  G -= Vd Z
+  for (int64_t j0 = 0; j0 < b; j0 += w) {
+    const int pw = static_cast<int>(std::min<int64_t>(w, b - j0));
+    MatView Vd{const_cast<double*>(D) + j0 * ldd, b, pw, ldd};
+    MatView Gv{G, b, nc, ldg};
+    QRB_TRY(gemm_tn(Vd, Gv, ws.W.d(), ldw, 0, pw, static_cast<int>(nc), static_cast<int>(b), 1,
+                    0, 0, st));
+    QRB_TRY(axpy_block(1.0, F + j0, ldf, ws.W.d(), ldw, pw, nc, st));
+    MatView Tv{const_cast<double*>(S) + j0, pw, pw, lds};
+    MatView Wv{ws.W.d(), pw, nc, ldw};
+    QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, pw, static_cast<int>(nc), pw, 1, 0, 0, st));
+    QRB_TRY(axpy_block(-1.0, ws.W2.d(), ldw, F + j0, ldf, pw, nc, st));
+    MatView W2v{ws.W2.d(), pw, nc, ldw};
+    QRB_TRY(gemm_nn(Vd, W2v, G, ldg, static_cast<int>(b), static_cast<int>(nc), pw, GEMM_EPI_SUB,
+                    0, st));
+    g_launches += 5;
+  }
+  return QRB_OK;
+}
+
 int qrb_copy_2d(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
                 int64_t cols, int kind, void* stream) {
   if (!dst || !src || rows < 0 || cols < 0 || ldd < rows || lds < rows || kind < 0 || kind > 3) {
