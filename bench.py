@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--cfg5-slices", type=int, default=4096,
                     help="slices of the config-5 solve-throughput run (0 = skip)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--lean-solve", action="store_true",
+                    help="multi-GPU: stream V and R instead of replicating the factors")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()

@@ -32,6 +32,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .errors import SingularMatrixError
+
 
 def owner_of(k: int, world: int) -> int:
     return k % world
@@ -78,6 +80,18 @@ class CudaOps:
         st = self.lib.qrb_op_apply_qt(self._p(v, v_off), ldv, m, w, self._p(t), ldt,
                                       self._p(c, c_off), ldc, nc, None)
         self.native.check(st, "qrb_op_apply_qt")
+
+    def trsm_upper(self, r, ldr, r_off, n, b, ldb, b_off, nrhs):
+        """b[b_off : b_off+n] <- R^-1 b for the n x n upper block starting at element r_off."""
+        st = self.lib.qrb_op_trsm_upper(self._p(r, r_off), ldr, n, 16,
+                                        self._p(b, b_off), ldb, nrhs, None)
+        self.native.check(st, "qrb_op_trsm_upper")
+
+    def gemm_nn_sub(self, a, lda, a_off, m, k, bmat, ldb, b_off, c, c_off, n):
+        """c[c_off : c_off+m] -= A (m x k at a + a_off) @ bmat[b_off : b_off+k]."""
+        st = self.lib.qrb_op_gemm_nn_sub(self._p(a, a_off), lda, self._p(bmat, b_off), ldb,
+                                         self._p(c, c_off), ldb, m, n, k, None)
+        self.native.check(st, "qrb_op_gemm_nn_sub")
 
     def sync(self):
         import torch
@@ -221,6 +235,62 @@ def gather_factored(f: DistFactors, group=None, place=None):
     return full
 
 
+def solve_distributed(f: DistFactors, b_share, ops, group=None):
+    """Memory-lean multi-GPU solve (no factor replication; config 4 at 8 GPUs):
+    every rank keeps only its own panels and solves its slice share b_share
+    (torch (s, lda), s may be 0).
+
+    Q^T B: panel by panel the owner broadcasts the packed reflector block
+    (same buffer as the factorization) and every rank applies it to its
+    slices.  R^-1: block column by block column from the bottom, the owner
+    broadcasts R[0:i1, block k]; every rank solves its diagonal block and
+    updates the rows above.  Traffic = one pass over V and R per solve, no
+    all-gather of the factored matrix.  Returns (x (s, n), resid (s,)).
+    """
+    import torch
+    import torch.distributed as dist
+
+    m, n, nb, lda, rank, world = f.m, f.n, f.nb, f.lda, f.rank, f.world
+    npan = -(-n // nb)
+    dev = f.a_local.device
+    s = b_share.shape[0]
+    y = b_share.clone()
+    buf = torch.empty((m + (m & 1)) * nb + nb * nb + nb, dtype=torch.float64, device=dev)
+    for k in range(npan):
+        j0, pw, mk, ldv, nelem, vview, tview, _ = _panel_views(buf, m, n, nb, k)
+        if rank == owner_of(k, world):
+            lcol = (k // world) * nb
+            vview[:, :mk].copy_(f.a_local[lcol:lcol + pw, j0:m])
+            tview.copy_(f.t_all[k * nb:(k + 1) * nb])
+        if world > 1:
+            dist.broadcast(buf[:nelem], src=owner_of(k, world), group=group)
+        if s:
+            ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, y, lda, j0, s)
+    resid = torch.linalg.norm(y[:, n:m], dim=1) if s else torch.zeros(0, device=dev)
+    rflat = torch.empty(nb * (n + 2), dtype=torch.float64, device=dev)
+    for k in range(npan - 1, -1, -1):
+        i0 = k * nb
+        bs = min(nb, n - i0)
+        i1 = i0 + bs
+        ldr = i1 + (i1 & 1)
+        rblk = rflat[: bs * ldr].view(bs, ldr)      # R[0:i1, block k], column-major, ld = ldr
+        if rank == owner_of(k, world):
+            lcol = (k // world) * nb
+            rblk[:, :i1].copy_(f.a_local[lcol:lcol + bs, :i1])
+        if world > 1:
+            dist.broadcast(rblk, src=owner_of(k, world), group=group)
+        diag = torch.diagonal(rblk[:, i0:i1]).cpu().numpy()
+        bad = np.flatnonzero(~(np.abs(diag) >= 1e-300))
+        if bad.size:
+            raise SingularMatrixError(i0 + int(bad[0]))
+        if s:
+            ops.trsm_upper(rblk, ldr, i0, bs, y, lda, i0, s)
+            if i0 > 0:
+                ops.gemm_nn_sub(rblk, ldr, 0, i0, bs, y, lda, i0, y, 0, s)
+    ops.sync()
+    return y[:, :n], resid
+
+
 def scatter_block_cyclic(a_full_cols, n: int, nb: int, rank: int, world: int):
     """This rank's local panels (torch (n_local, lda)) from a full (n, lda) tensor."""
     import torch
@@ -279,12 +349,21 @@ def bench_rank(args, rank: int, world: int):
     x_dev = torch.zeros((max(cnt, 1), n + (n & 1)), dtype=torch.float64, device="cuda")
     ops = CudaOps()
     a_local = torch.empty_like(a_pristine)
-    q = QrDevice(m, n, nb)
+    # replicate the factors for the solve only if a full copy (plus the gather
+    # buffer) fits next to the local panels; otherwise stream V and R (config 4)
+    free, total = torch.cuda.mem_get_info()
+    lean = args.lean_solve or 2 * 8 * lda * n > 0.8 * free
+    q = None if lean else QrDevice(m, n, nb)
 
     def step():
         a_local.copy_(a_pristine)
         f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
         t1 = time.perf_counter()
+        if lean:
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            solve_distributed(f, b_dev[:cnt], ops)
+            return f.factor_seconds, 0.0, time.perf_counter() - ts
         gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
         q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
         t2 = time.perf_counter()
@@ -330,10 +409,15 @@ def bench_rank(args, rank: int, world: int):
     t_e2e = time.perf_counter()
     a_local.copy_(a_pin, non_blocking=True)
     f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
-    gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
-    q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
-    if cnt:
-        q.solve(b_pin.numpy().T[:m, :cnt], out=x_pin.numpy().T[:, :cnt])
+    if lean:
+        b_dev[:cnt].copy_(b_pin[:cnt], non_blocking=True)
+        xs, _ = solve_distributed(f, b_dev[:cnt], ops)
+        x_pin[:cnt].copy_(xs)
+    else:
+        gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
+        q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+        if cnt:
+            q.solve(b_pin.numpy().T[:m, :cnt], out=x_pin.numpy().T[:, :cnt])
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t_e2e], device="cuda")
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -352,6 +436,8 @@ def bench_rank(args, rank: int, world: int):
             "slices_per_s": S / float(s_s),
             "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,
             "factor_ms": float(f_s) * 1e3, "gather_ms": float(np.mean(gs)) * 1e3,
+            "solve_path": "streamed V/R broadcast (no replication)" if lean else
+                          "all-gathered factors, per-rank solve",
             "gpu_launches": int(launches), "clocks": clocks,
             "e2e": {"value": fl / float(e2e_s) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * lda * n + 8 * m * S),

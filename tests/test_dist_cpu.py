@@ -47,6 +47,17 @@ class NumpyOps:
         cm = strided(c, c_off, m, nc, ldc)
         cm -= vu @ (tf.T @ (vu.T @ cm))
 
+    def trsm_upper(self, r, ldr, r_off, n, b, ldb, b_off, nrhs):
+        rm = np.triu(strided(r, r_off, n, n, ldr).copy())
+        bm = strided(b, b_off, n, nrhs, ldb)
+        bm[:, :] = np.linalg.solve(rm, bm)
+
+    def gemm_nn_sub(self, a, lda, a_off, m, k, bmat, ldb, b_off, c, c_off, n):
+        am = strided(a, a_off, m, k, lda).copy()
+        bm = strided(bmat, b_off, k, n, ldb).copy()
+        cm = strided(c, c_off, m, n, ldb)
+        cm -= am @ bm
+
     def sync(self):
         pass
 
@@ -87,6 +98,11 @@ def worker(rank, world, port, m, n, nb, out_dir, lookahead=True):
         c[j0:] -= vu @ (tf.T @ (vu.T @ c[j0:]))
     x = np.linalg.solve(np.triu(fm[:n, :n]), c[:n])
     np.save(os.path.join(out_dir, f"x_{rank}.npy"), x)
+    # memory-lean solve: panels and R block columns broadcast, no gather
+    bsh = torch.zeros((cnt, lda), dtype=torch.float64)
+    bsh[:, :m] = torch.from_numpy(np.ascontiguousarray(bmat[:, first:first + cnt].T))
+    x2, r2 = qd.solve_distributed(f, bsh, NumpyOps())
+    np.save(os.path.join(out_dir, f"x2_{rank}.npy"), x2.numpy().T)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -114,6 +130,8 @@ def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb, la
         assert parts[-1].shape == (n, cnt)
     x = np.concatenate(parts, axis=1)
     assert np.abs(x - x_ref).max() <= 1e-8 * np.abs(x_ref).max()
+    x2 = np.concatenate([np.load(tmp_path / f"x2_{r_}.npy") for r_ in range(world)], axis=1)
+    assert np.abs(x2 - x_ref).max() <= 1e-8 * np.abs(x_ref).max()
 
 
 def test_ownership_helpers():

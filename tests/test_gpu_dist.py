@@ -46,5 +46,11 @@ def test_single_rank_nccl_factor_gather_solve():
         x, _, _ = q.solve(bm)
         assert rel_err(x, orc.solve_dense(ref, bm)) <= 1e-8
         q.close()
+        # memory-lean solve straight from the distributed factors
+        bsh = torch.zeros((5, lda), dtype=torch.float64, device="cuda")
+        bsh[:, :m] = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda()
+        x2, r2 = qd.solve_distributed(f, bsh, qd.CudaOps())
+        assert rel_err(x2.cpu().numpy().T, orc.solve_dense(ref, bm)) <= 1e-8
+        np.testing.assert_allclose(r2.cpu().numpy(), orc.residual_norms(ref, bm), rtol=1e-9)
     finally:
         dist.destroy_process_group()
