@@ -194,6 +194,19 @@ def densify_device(g: FanGeometry, lda: int | None = None, rank: int = 0, world:
     """Dense column-major A (or this rank's block-cyclic panels) built on the GPU
     by the sm_100a Siddon kernel (qrb_siddon_densify); returns a torch tensor of
     shape (local columns, lda).  Bit-identical to :func:`dense_matrix`."""
+    import torch
+
+    m, n = g.n_rays, g.n_pixels
+    lda = lda or (m + 31) // 32 * 32
+    npan = -(-n // nb)
+    n_local = sum(min(nb, n - k * nb) for k in range(rank, npan, world)) if world > 1 else n
+    a = torch.zeros((n_local, lda), dtype=torch.float64, device="cuda")
+    return densify_into(g, a, lda, rank, world, nb, views_per_call)
+
+
+def densify_into(g: FanGeometry, a, lda: int, rank: int = 0, world: int = 1, nb: int = 128,
+                 views_per_call: int = 64):
+    """Write the Siddon weights into an already zeroed device tensor (cols, lda)."""
     import ctypes
 
     import torch
@@ -201,11 +214,7 @@ def densify_device(g: FanGeometry, lda: int | None = None, rank: int = 0, world:
     from . import _native
 
     lib = _native.load()
-    m, n = g.n_rays, g.n_pixels
-    lda = lda or (m + 31) // 32 * 32
-    npan = -(-n // nb)
-    n_local = sum(min(nb, n - k * nb) for k in range(rank, npan, world)) if world > 1 else n
-    a = torch.zeros((n_local, lda), dtype=torch.float64, device="cuda")
+    n_local = a.shape[0]
     for v0 in range(0, g.views, views_per_call):
         views = np.arange(v0, min(g.views, v0 + views_per_call))
         ends = np.stack([e.ravel() for e in ray_endpoints(g, views)])  # (4, rays)

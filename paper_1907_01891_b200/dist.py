@@ -348,7 +348,18 @@ def bench_rank(args, rank: int, world: int):
     b_dev[:cnt, :m] = torch.from_numpy(np.ascontiguousarray(b_host[:, first:first + cnt].T)).cuda()
     x_dev = torch.zeros((max(cnt, 1), n + (n & 1)), dtype=torch.float64, device="cuda")
     ops = CudaOps()
-    a_local = torch.empty_like(a_pristine)
+    # keep a pristine copy of the local panels only if it fits (config 4 at 8 GPUs
+    # is ~71 GB per rank: re-densify with the Siddon kernel instead)
+    free, total = torch.cuda.mem_get_info()
+    if 8 * a_pristine.numel() < 0.4 * free:
+        a_local = torch.empty_like(a_pristine)
+        reset = lambda: a_local.copy_(a_pristine)  # noqa: E731
+    else:
+        a_local, a_pristine = a_pristine, None
+
+        def reset():
+            a_local.zero_()
+            cs.densify_into(g, a_local, lda, rank=rank, world=world, nb=nb)
     # replicate the factors for the solve only if a full copy (plus the gather
     # buffer) fits next to the local panels; otherwise stream V and R (config 4)
     free, total = torch.cuda.mem_get_info()
@@ -356,7 +367,7 @@ def bench_rank(args, rank: int, world: int):
     q = None if lean else QrDevice(m, n, nb)
 
     def step():
-        a_local.copy_(a_pristine)
+        reset()
         f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
         t1 = time.perf_counter()
         if lean:
@@ -399,8 +410,9 @@ def bench_rank(args, rank: int, world: int):
 
     # end to end through host buffers: this rank's panels from pinned host memory
     # in, its slice share of X out (factorization + gather + solve inside)
-    a_pin = torch.empty(a_pristine.shape, dtype=torch.float64, pin_memory=True)
-    a_pin.copy_(a_pristine)
+    reset()
+    a_pin = torch.empty(a_local.shape, dtype=torch.float64, pin_memory=True)
+    a_pin.copy_(a_local)
     b_pin = torch.empty((max(cnt, 1), lda), dtype=torch.float64, pin_memory=True)
     b_pin.copy_(b_dev)
     x_pin = torch.empty((max(cnt, 1), n), dtype=torch.float64, pin_memory=True)
@@ -443,8 +455,9 @@ def bench_rank(args, rank: int, world: int):
                     "h2d_bytes_per_step": int(8 * lda * n + 8 * m * S),
                     "d2h_bytes_per_step": int(8 * n * S),
                     "ms_per_step": float(e2e_s) * 1e3,
-                    "path": "pinned host panels -> factorize_distributed -> all-gather -> "
-                            "QrDevice.solve(host B share -> host X share); max over ranks"},
+                    "path": "pinned host panels -> factorize_distributed -> " +
+                            ("streamed V/R solve" if lean else "all-gather -> QrDevice.solve") +
+                            " (host B share -> host X share); max over ranks"},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
