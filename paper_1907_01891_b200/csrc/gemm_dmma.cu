@@ -577,6 +577,158 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 
 // ---------------------------------------------------------------------------
+// persistent C -= A B with an ASYNCHRONOUS L2 reduce-add epilogue: the eight
+// consumer warps stage -acc into one of two padded shared-memory buffers and
+// only *arrive* on an mbarrier; a dedicated epilogue warp waits for the staged
+// tile and issues the 64 per-column cp.reduce.async.bulk .add.f64 reductions,
+// releasing the buffer when the bulk reads are done.  The consumers go straight
+// back to the DMMA main loop of the next tile (no named barrier in their path).
+// ---------------------------------------------------------------------------
+constexpr int AE_STAGES = 6;
+constexpr int AE_SBUF = 1;  // staging buffers (the bulk read of one finishes long before the next tile)
+constexpr int AE_THREADS = (CONSUMER_WARPS + 2) * 32;  // + producer warp + epilogue warp
+constexpr int AE_SMEM = AE_STAGES * NN_STAGE_BYTES + AE_SBUF * RA_STAGING + 1024 + 256;
+
+__global__ void __launch_bounds__(AE_THREADS, 1)
+    gemm_nn_sub_asyncepi(const __grid_constant__ CUtensorMap mapA,
+                         const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
+                         const int64_t ldc, const NnArgs args) {
+  constexpr int NT = NN_BN / 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stage0 = smem + AE_STAGES * NN_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + AE_SBUF * RA_STAGING);
+  uint64_t* empty = full + AE_STAGES;
+  uint64_t* sfull = empty + AE_STAGES;
+  uint64_t* sempty = sfull + 2;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + NN_BN - 1) / NN_BN;
+  const int num_k = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AE_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sfull[b], CONSUMER_WARPS);
+      mbar_init(&sempty[b], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {  // ---- TMA producer ----
+    if (lane == 0) {
+      prefetch_tmap(&mapA);
+      prefetch_tmap(&mapB);
+      int kit = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+        for (int kt = 0; kt < num_k; ++kt, ++kit) {
+          const int s = kit % AE_STAGES;
+          if (kit >= AE_STAGES) mbar_wait(&empty[s], ((kit / AE_STAGES) & 1) ^ 1);
+          uint8_t* sA = smem + s * NN_STAGE_BYTES;
+          uint8_t* sB = sA + NN_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], NN_STAGE_BYTES);
+          const int k = kt * BK;
+#pragma unroll
+          for (int mb = 0; mb < BM / 16; ++mb)
+            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+          tma_load_2d(sB, &mapB, k, n_tile * NN_BN, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == CONSUMER_WARPS + 1) {  // ---- epilogue warp: bulk L2 reductions ----
+    int it = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      int m_tile, n_tile;
+      decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+      const int sb = it % AE_SBUF;
+      const int mg0 = m_tile * BM, ng0 = n_tile * NN_BN;
+      mbar_wait(&sfull[sb], (it / AE_SBUF) & 1);
+      const uint8_t* stage = stage0 + sb * RA_STAGING;
+      const int rows = min(BM, args.M - mg0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = lane + 32 * h;
+        if (ng0 + n < args.N && rows > 0) {
+          double* dst = C + mg0 + static_cast<int64_t>(ng0 + n) * ldc;
+          const int even = rows & ~1;
+          if (even) bulk_reduce_add_f64(dst, stage + n * RA_COL_BYTES, even * 8);
+          if (rows & 1)
+            atomicAdd(dst + even,
+                      *reinterpret_cast<const double*>(stage + n * RA_COL_BYTES + even * 8));
+        }
+      }
+      bulk_commit();
+      bulk_wait_read0();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sb]);
+    }
+    bulk_wait0();
+    return;
+  }
+
+  // ---- consumer warps: DMMA main loop, stage -acc, arrive ----
+  const int g = lane >> 2;
+  const int q = lane & 3;
+  const int m0 = (warp & 3) * 32;
+  const int n0 = (warp >> 2) * (NN_BN / 2);
+  int kit = 0, it = 0;
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    int m_tile, n_tile;
+    decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+    const int mg0 = m_tile * BM;
+    const int ng0 = n_tile * NN_BN;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < num_k; ++kt, ++kit) {
+      const int s = kit % AE_STAGES;
+      mbar_wait(&full[s], (kit / AE_STAGES) & 1);
+      const uint8_t* sA = smem + s * NN_STAGE_BYTES;
+      const uint8_t* sB = sA + NN_A_BYTES;
+      const int kg0 = kt * BK;
+      if (args.mask_a && mg0 <= kg0 + BK - 1)
+        consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else
+        consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const int sb = it % AE_SBUF;
+    if (it >= AE_SBUF) mbar_wait(&sempty[sb], ((it / AE_SBUF) - 1) & 1);
+    uint8_t* stage = stage0 + sb * RA_STAGING;
+#pragma unroll
+    for (int mp = 0; mp < 2; ++mp) {
+      const int m = m0 + mp * 16 + 2 * g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + nt * 8 + rp(2 * q + e);
+          *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
+              make_double2(-acc[mp * 2 + 0][nt][e], -acc[mp * 2 + 1][nt][e]);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sfull[sb]);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -720,6 +872,32 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   if ((reinterpret_cast<uintptr_t>(out) & 15) != 0 || (ldo & 1) != 0) {
     set_last_error("gemm_nn: output must be 16-byte aligned with even ld");
     return QRB_ERR_ARG;
+  }
+  static const bool asyncepi = std::getenv("QRB_NN_SYNC_EPI") == nullptr;
+  if (epi == GEMM_EPI_SUB && asyncepi && !(std::getenv("QRB_NN_STAGED_C")) &&
+      !(std::getenv("QRB_NN_CLASSIC"))) {
+    static bool configured_ae = false;
+    if (!configured_ae) {
+      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_asyncepi,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, AE_SMEM));
+      configured_ae = true;
+    }
+    CUtensorMap ma, mb;
+    QRB_TRY(make_map(&ma, a_mm, 16, BK));
+    QRB_TRY(make_map(&mb, b, BK, NN_BN));
+    NnArgs args;
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.mask_a = mask_a;
+    args.group_m = 16;
+    const int num_m = (M + BM - 1) / BM;
+    const int num_n = (N + NN_BN - 1) / NN_BN;
+    args.num_tiles = num_m * num_n;
+    const int grid = std::min(args.num_tiles, gemm_sm_count());
+    gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
+    QRB_CUDA_TRY(cudaGetLastError());
+    return QRB_OK;
   }
   static const bool redadd = std::getenv("QRB_NN_STAGED_C") == nullptr;
   if (epi == GEMM_EPI_SUB && redadd && !(std::getenv("QRB_NN_CLASSIC"))) {
