@@ -268,6 +268,14 @@ def ours_arm(args, rank: int, world: int):
     resid_rel = float((torch.abs(r_explicit - r_dev) / r_explicit).max())
     resid_dbg = {"explicit": r_explicit[:3].tolist(), "identity": r_dev[:3].tolist(),
                  "x_absmax": float(x_last.abs().max())}
+    # image quality of the reconstructed slices vs the phantoms (paper Tables IV/V metrics)
+    from paper_1907_01891_b200 import metrics
+    xt_dev = torch.from_numpy(x_true).cuda()
+    quality = {"psnr_avg_db": float(metrics.psnr(xt_dev, x_last.T, g.image_pixels).mean()),
+               "ssim_avg": float(metrics.ssim(xt_dev, x_last.T, g.image_pixels).mean()),
+               "relative_residual": metrics.relative_residual(a_dev, x_last.T, b_dev[:, :m].T, m),
+               "note": "noisy sinograms (1% Gaussian), least-squares solution"}
+    del xt_dev
 
     # config 5: solve throughput of a 4096-slice batch against the config-3 factors
     cfg5 = None
@@ -345,7 +353,7 @@ def ours_arm(args, rank: int, world: int):
                          "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
                                    f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
-        "config5": cfg5,
+        "config5": cfg5, "quality": quality,
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s, "densify_s": densify_s,
     }

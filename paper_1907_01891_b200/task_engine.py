@@ -61,6 +61,7 @@ class EngineConfig:
     prefetch_depth: int = 2
     panel_width: int = 128
     device: int = 0
+    hbm_budget_bytes: int = 0  # 0 = 85% of free HBM; above it A is host-staged (ooc.py)
 
     def validate(self) -> "EngineConfig":
         if self.tile_size < 1:
@@ -82,6 +83,8 @@ class EngineConfig:
         if self.panel_width % 16 or not 16 <= self.panel_width <= 128:
             raise ValueError(f"panel_width must be a multiple of 16 in [16, 128], "
                              f"got {self.panel_width}")
+        if self.hbm_budget_bytes < 0:
+            raise ValueError("hbm_budget_bytes must be >= 0")
         return self
 
     def min_cache_tiles(self) -> int:
@@ -162,6 +165,7 @@ class QrFactors:
     geometry_hash: str = ""
     directory: Path | None = None
     device_state: QrDevice | None = field(default=None, repr=False, compare=False)
+    host_state: object = field(default=None, repr=False, compare=False)  # ooc.HostStagedQR
 
     @property
     def grid_rows(self) -> int:
@@ -264,6 +268,71 @@ def _factor_dir_writes(factors: QrFactors, dev: QrDevice, directory: Path) -> tu
     return time.perf_counter() - t0, written
 
 
+def _hbm_budget(cfg: EngineConfig) -> int:
+    if cfg.hbm_budget_bytes:
+        return int(cfg.hbm_budget_bytes)
+    import torch
+    free, _ = torch.cuda.mem_get_info(cfg.device)
+    return int(0.85 * free)
+
+
+def _fits_in_hbm(rows: int, cols: int, cfg: EngineConfig) -> bool:
+    lda = (rows + 31) // 32 * 32
+    # matrix + T/R^-1 blocks + workspaces (~1 GB)
+    return 8 * lda * cols + (1 << 30) <= _hbm_budget(cfg)
+
+
+def _pinned_from_tiles(store: TiledMatrix, rows: int, cols: int):
+    """(n, lda) pinned host tensor (column-major m x n) filled from a tile store."""
+    import torch
+    lda = (rows + 31) // 32 * 32
+    host = torch.zeros((cols, lda), dtype=torch.float64, pin_memory=True)
+    view = host.numpy().T            # lda x cols, Fortran
+    b = store.tile_size
+    for j in range(store.grid_cols):
+        try:
+            store.read_column_block(j, view[:rows, j * b:j * b + min(b, cols - j * b)])
+        except (OSError, CorruptTileError) as exc:
+            raise TaskIoError(j * store.grid_rows, "stage", exc) from exc
+    return host
+
+
+def _factorize_host_staged(a: TiledMatrix, cfg: EngineConfig, factors_dir: Path,
+                           geometry_hash: str) -> tuple["QrFactors", RunReport]:
+    from .ooc import HostStagedQR
+    t_start = time.perf_counter()
+    t0 = time.perf_counter()
+    host = _pinned_from_tiles(a, a.rows, a.cols)
+    t_read = time.perf_counter() - t0
+    q = HostStagedQR(host, a.rows, a.cols, nb=cfg.panel_width, budget_bytes=_hbm_budget(cfg))
+    st = q.factorize()
+    b = a.tile_size
+    factored = TiledMatrix.create(a.rows, a.cols, b, factors_dir / "factored")
+    factors = QrFactors(factored=factored, inner_block=cfg.inner_block, rows=a.rows,
+                        cols=a.cols, tile_size=b, panel_width=cfg.panel_width,
+                        geometry_hash=geometry_hash, directory=factors_dir)
+    t1 = time.perf_counter()
+    view = host.numpy().T
+    written = 0
+    for j in range(factored.grid_cols):
+        written += factored.write_column_block(j, view[:a.rows, j * b:j * b + min(b, a.cols - j * b)])
+    q.tau.cpu().numpy()[:a.cols].astype("<f8").tofile(factors_dir / _TAU_NAME)
+    q.t_all.cpu().numpy().T.astype("<f8").ravel(order="F").tofile(factors_dir / _T_NAME)
+    t_write = time.perf_counter() - t1
+    factors.save_meta(factors_dir)
+    factors.host_state = q
+    report = RunReport(
+        mode=cfg.mode, task_count=0, total_seconds=time.perf_counter() - t_start,
+        compute_seconds=st["seconds"], io_read_seconds=t_read, io_write_seconds=t_write,
+        tiles_read=a.grid_rows * a.grid_cols, tiles_written=written, cache_hits=0,
+        trace=[TaskTrace(0, "stage_a_pinned", 0.0, t_read * 1e3, 0.0),
+               TaskTrace(1, "qr_host_staged_superpanels", st["seconds"] * 1e3, 0.0, 0.0),
+               TaskTrace(2, "write_factors", 0.0, 0.0, t_write * 1e3)],
+        gpu_flops=2.0 * a.rows * a.cols ** 2 - 2.0 * a.cols ** 3 / 3.0,
+        h2d_seconds=0.0)
+    return factors, report
+
+
 def factorize(a: TiledMatrix, config: EngineConfig, factors_dir,
               geometry_hash: str = "", keep_on_device: bool = True) -> tuple[QrFactors, RunReport]:
     """QR-factor a tiled matrix on the GPU; ``a`` itself is left untouched.
@@ -279,6 +348,8 @@ def factorize(a: TiledMatrix, config: EngineConfig, factors_dir,
         raise ValueError(f"config tile_size {cfg.tile_size} != matrix tile_size {a.tile_size}")
     factors_dir = Path(factors_dir)
     factors_dir.mkdir(parents=True, exist_ok=True)
+    if not _fits_in_hbm(a.rows, a.cols, cfg):
+        return _factorize_host_staged(a, cfg, factors_dir, geometry_hash)
     t_start = time.perf_counter()
     dev = QrDevice(a.rows, a.cols, cfg.panel_width, cfg.device)
     b = a.tile_size
@@ -343,6 +414,9 @@ def solve(factors: QrFactors, b_mat: TiledMatrix, config: EngineConfig,
     factors.check_complete()
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
+    if factors.host_state is not None or (factors.device_state is None and
+                                          not _fits_in_hbm(factors.rows, factors.cols, cfg)):
+        return _solve_host_staged(factors, b_mat, cfg, out_dir)
     t_start = time.perf_counter()
     dev, t_read_f, t_h2d_f, tiles_f = factors.to_device(cfg.device)
     b = b_mat.tile_size
@@ -371,6 +445,52 @@ def solve(factors: QrFactors, b_mat: TiledMatrix, config: EngineConfig,
         tiles_read=tiles_f + b_mat.grid_rows * b_mat.grid_cols, tiles_written=written,
         cache_hits=0, trace=trace, gpu_flops=rep["flops"],
         h2d_seconds=t_h2d_f + rep["h2d_ms"] / 1e3, d2h_seconds=rep["d2h_ms"] / 1e3)
+    return xm, report
+
+
+def _solve_host_staged(factors: "QrFactors", b_mat: TiledMatrix, cfg: EngineConfig,
+                       out_dir: Path) -> tuple[TiledMatrix, RunReport]:
+    import torch
+
+    from .ooc import HostStagedQR
+    t_start = time.perf_counter()
+    q = factors.host_state
+    if q is None:
+        host = _pinned_from_tiles(factors.factored, factors.rows, factors.cols)
+        q = HostStagedQR(host, factors.rows, factors.cols, nb=factors.panel_width,
+                         budget_bytes=_hbm_budget(cfg))
+        npan = -(-factors.cols // factors.panel_width)
+        nb = factors.panel_width
+        tau = np.fromfile(factors.directory / _TAU_NAME, dtype="<f8")
+        t = np.fromfile(factors.directory / _T_NAME, dtype="<f8").reshape((nb, npan * nb),
+                                                                          order="F")
+        q.tau[:factors.cols] = torch.from_numpy(tau).cuda()
+        q.t_all.copy_(torch.from_numpy(np.ascontiguousarray(t.T)).cuda())
+        factors.host_state = q
+    lda = q.lda
+    bm = np.empty((b_mat.rows, b_mat.cols), order="F")
+    b = b_mat.tile_size
+    try:
+        for j in range(b_mat.grid_cols):
+            b_mat.read_column_block(j, bm[:, j * b:j * b + min(b, b_mat.cols - j * b)])
+    except (OSError, CorruptTileError, CacheCapacityError) as exc:
+        raise TaskIoError(0, "stage_b", exc) from exc
+    b_dev = torch.zeros((b_mat.cols, lda), dtype=torch.float64, device="cuda")
+    b_dev[:, :b_mat.rows] = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda()
+    t0 = time.perf_counter()
+    x, _ = q.solve(b_dev, report_block=factors.tile_size)
+    t_compute = time.perf_counter() - t0
+    x = x.cpu().numpy().T
+    xm = TiledMatrix.create(factors.cols, b_mat.cols, b, out_dir / "x")
+    written = 0
+    for j in range(xm.grid_cols):
+        written += xm.write_column_block(j, x[:, j * b:j * b + min(b, b_mat.cols - j * b)])
+    report = RunReport(
+        mode=cfg.mode, task_count=0, total_seconds=time.perf_counter() - t_start,
+        compute_seconds=t_compute, io_read_seconds=0.0, io_write_seconds=0.0,
+        tiles_read=b_mat.grid_rows * b_mat.grid_cols, tiles_written=written, cache_hits=0,
+        trace=[TaskTrace(0, "host_staged_solve", t_compute * 1e3, 0.0, 0.0)],
+        gpu_flops=(4.0 * factors.rows * factors.cols - factors.cols ** 2) * b_mat.cols)
     return xm, report
 
 
