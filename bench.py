@@ -260,6 +260,7 @@ def ours_arm(args, rank: int, world: int):
                 "peak_source": FP64_PEAK_SOURCE,
                 "per_launch_flops": dk["flops"] / dk["launches"],
                 "avg_launch_ms": dk["ms"] / dk["launches"]}
+    roofline.update(_ncu_traffic(dom, m, n, args.nb))
     shares = {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4) for k, v in kstats.items()}
 
     # residual sanity of the last step: GPU residual identity vs explicit ||Ax - b||
@@ -358,6 +359,29 @@ def ours_arm(args, rank: int, world: int):
         "setup_s": setup_s, "densify_s": densify_s,
     }
     print(json.dumps(line), flush=True)
+
+
+def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
+    """DRAM bytes of the dominant kernel from the committed `ncu --set full`
+    capture (profiles/r01_ncu_full_gemm_nn_config3.txt: the k = 0 launch of the
+    config-3 NN update C -= V W2, C = m x (n - nb), V = m x nb, W2 = nb x (n - nb)).
+    Read from the committed summary, not measured in this run."""
+    prof = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_gemm_nn_config3.txt"
+    if kernel != "gemm_nn" or (m, n) != (69120, 65536) or not prof.is_file():
+        return {}
+    vals = {}
+    for line in prof.read_text().splitlines():
+        parts = line.split(",")
+        if len(parts) >= 2 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            vals[parts[0]] = float(parts[1]) * 1e9
+    if len(vals) != 2:
+        return {}
+    nc = n - nb
+    algo = 8.0 * (2 * m * nc + m * nb + nb * nc)
+    return {"traffic": sum(vals.values()), "traffic_unit": "bytes",
+            "traffic_launch": f"k=0 launch ({m}x{nc}x{nb}), ncu --set full, "
+                              "profiles/r01_ncu_full_gemm_nn_config3.txt",
+            "traffic_algorithmic": algo}
 
 
 def main():

@@ -206,6 +206,16 @@ QRB_API int64_t qrb_launch_count(void);
 /* Release all library workspaces of the current device. */
 QRB_API int qrb_release_workspace(void);
 
+/* Process-wide tuning knobs and counters (no reference counterpart: the
+ * reference's only backend switch is kernels.use_path, kernels.py:265-283).
+ *   "panel_algo"       0 auto | 1 Householder columns | 2 CholeskyQR2 when the shape allows
+ *   "cholqr_min_rows"  auto mode uses CholeskyQR2 for panels with at least this many rows
+ *   "cholqr_panels"    (read only) panels that tried the CholeskyQR2 route
+ *   "cholqr_fallbacks" (read only) of those, panels that fell back to Householder columns
+ * qrb_set_tuning returns QRB_ERR_ARG for an unknown or read-only key. */
+QRB_API int qrb_set_tuning(const char* key, int64_t value);
+QRB_API int qrb_get_tuning(const char* key, int64_t* value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,8 @@ SIGNATURES = {
     "qrb_copy_2d": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_i64, c_i64, c_int, c_void_p]),
     "qrb_launch_count": (c_i64, []),
     "qrb_release_workspace": (c_int, []),
+    "qrb_set_tuning": (c_int, [ctypes.c_char_p, c_i64]),
+    "qrb_get_tuning": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_i64)]),
 }
 
 _lib = None
@@ -147,3 +149,14 @@ def check(status: int, what: str) -> int:
             raise KernelInputError(msg)
         raise GpuError(msg)
     return status
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Process-wide knob of the native library (qrb_set_tuning)."""
+    check(load().qrb_set_tuning(key.encode(), int(value)), f"qrb_set_tuning({key})")
+
+
+def get_tuning(key: str) -> int:
+    out = c_i64(0)
+    check(load().qrb_get_tuning(key.encode(), ctypes.byref(out)), f"qrb_get_tuning({key})")
+    return int(out.value)

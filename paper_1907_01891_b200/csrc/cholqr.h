@@ -1,0 +1,24 @@
+// Internal C++ interface of the CholeskyQR2 panel pieces (see cholqr.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qrb {
+
+// R = chol(G) (upper), Rinv = R^-1; b <= 128, outputs b x b with leading dim ldo.
+// Raises `bit` in *flag on a non-positive pivot, a non-finite inverse, or (when
+// check_identity) ||G - I||_F > 1/2.
+int chol_inv(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, int* flag, int bit,
+             int check_identity, cudaStream_t stream);
+
+// LU without pivoting of Qt - diag(s), s_k = -sign(current pivot):
+// Uc, NUcS = -Uc diag(s), L1 (strict lower), Ucinv, L1invT = L1^-T, s.
+int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, double* L1,
+                double* Ucinv, double* L1invT, double* s, int ldo, int* flag, int bit,
+                cudaStream_t stream);
+
+// P[0:b,0:b] <- diag(s) R on/above the diagonal, L1 below; tau_k = T_kk.
+int cholqr_write_top(double* P, int64_t ldp, int b, const double* R, const double* s,
+                     const double* L1, const double* T, int64_t ldt, double* tau, int ldo,
+                     cudaStream_t stream);
+
+}  // namespace qrb

@@ -10,6 +10,7 @@
 // writes (task_engine.py:187-254); with the matrix resident in HBM the
 // B200-native order is right-looking by panels of nb columns, every trailing
 // update being two large DMMA GEMMs.
+#include "cholqr.h"
 #include "common.cuh"
 #include "gemm.h"
 #include "panel.h"
@@ -63,7 +64,14 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf part, bar, G, Ti, W, W2, Wparts;
+  DevBuf Wq, small, flag;  // CholeskyQR2 panel: Q1 (m x b), 12 b x b blocks, status word
+  int* hflag = nullptr;    // pinned host copy of the status word
   void release() {
+    if (hflag) cudaFreeHost(hflag);
+    hflag = nullptr;
+    Wq.release();
+    small.release();
+    flag.release();
     part.release();
     bar.release();
     G.release();
@@ -201,6 +209,103 @@ static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ld
   return factor_panel_impl(panel, tau, T, ldt, ws, st);
 }
 
+// Panel algorithm selection (qrb_set_tuning): 0 = auto (CholeskyQR2 +
+// reconstruction for tall panels, Householder columns otherwise),
+// 1 = Householder columns always, 2 = CholeskyQR2 whenever the shape allows.
+static int g_panel_algo = [] {
+  const char* e = std::getenv("QRB_PANEL_ALGO");
+  return e ? std::atoi(e) : 0;
+}();
+static int64_t g_cholqr_min_rows = 4096;
+static std::atomic<int64_t> g_cholqr_panels{0}, g_cholqr_fallbacks{0};
+
+// CholeskyQR2 + Householder reconstruction of an m x b panel (cholqr.cu header
+// for the algebra).  Returns QRB_OK with *done = false, the panel untouched,
+// when the Cholesky route is not trustworthy for this panel (caller falls
+// back to the column-by-column Householder kernel).
+static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, int64_t ldt,
+                                Workspace& ws, cudaStream_t st, bool* done) {
+  *done = false;
+  const int m = static_cast<int>(panel.rows);
+  const int b = static_cast<int>(panel.cols);
+  const int64_t mw = (static_cast<int64_t>(m) + 1) & ~int64_t(1);
+  constexpr int LD = 128;
+  constexpr int64_t BLK = int64_t(LD) * LD;
+  QRB_TRY(ws.Wq.ensure(sizeof(double) * mw * b, st));
+  QRB_TRY(ws.small.ensure(sizeof(double) * (BLK * 13 + LD), st));
+  QRB_TRY(ws.flag.ensure(64, st));
+  QRB_TRY(ws.G.ensure(sizeof(double) * LD * 128, st));
+  if (!ws.hflag) QRB_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ws.hflag), 64));
+  double* sb = ws.small.d();
+  double *R1 = sb, *R1i = sb + BLK, *R2 = sb + 2 * BLK, *R2i = sb + 3 * BLK, *Qt = sb + 4 * BLK;
+  double *Uc = sb + 5 * BLK, *NUcS = sb + 6 * BLK, *L1 = sb + 7 * BLK, *Uci = sb + 8 * BLK;
+  double *L1iT = sb + 9 * BLK, *M = sb + 10 * BLK, *R = sb + 11 * BLK, *Tt = sb + 12 * BLK;
+  double* s = sb + 13 * BLK;
+  int* flag = static_cast<int*>(ws.flag.p);
+  double* Wq = ws.Wq.d();
+  QRB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  auto gram = [&](const MatView& X) -> int {
+    const int64_t per = int64_t(LD) * b;
+    const int splits = gemm_pick_splits(b, b, m, 64);
+    if (splits > 1) {
+      QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+      int used = 0;
+      QRB_TRY(gemm_tn_split(X, X, ws.Wparts.d(), LD, per, b, b, m, splits, 0, 0, st, &used));
+      QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, b, b, LD, ws.G.d(), LD, st));
+      g_launches += 2;
+    } else {
+      QRB_TRY(gemm_tn(X, X, ws.G.d(), LD, 0, b, b, m, 1, 0, 0, st));
+      g_launches += 1;
+    }
+    return QRB_OK;
+  };
+  const MatView Q1{Wq, m, b, mw};
+  // pass 1: G1 = P^T P, R1 = chol(G1), Q1 = P R1^-1
+  QRB_TRY(gram(panel));
+  QRB_TRY(chol_inv(ws.G.d(), LD, b, R1, R1i, LD, flag, 1, 0, st));
+  QRB_TRY(gemm_nn(panel, MatView{R1i, b, b, LD}, Wq, mw, m, b, b, GEMM_EPI_STORE, 0, st));
+  // pass 2: G2 = Q1^T Q1 (must be close to I), R2 = chol(G2)
+  QRB_TRY(gram(Q1));
+  QRB_TRY(chol_inv(ws.G.d(), LD, b, R2, R2i, LD, flag, 2, 1, st));
+  // top block of Q = Q1 R2^-1, modified LU, small products
+  QRB_TRY(gemm_nn(MatView{Wq, b, b, mw}, MatView{R2i, b, b, LD}, Qt, LD, b, b, b, GEMM_EPI_STORE,
+                  0, st));
+  QRB_TRY(modified_lu(Qt, LD, b, Uc, NUcS, L1, Uci, L1iT, s, LD, flag, 4, st));
+  QRB_TRY(gemm_nn(MatView{R2i, b, b, LD}, MatView{Uci, b, b, LD}, M, LD, b, b, b, GEMM_EPI_STORE,
+                  0, st));
+  QRB_TRY(gemm_nn(MatView{R2, b, b, LD}, MatView{R1, b, b, LD}, R, LD, b, b, b, GEMM_EPI_STORE, 0,
+                  st));
+  QRB_TRY(gemm_nn(MatView{NUcS, b, b, LD}, MatView{L1iT, b, b, LD}, Tt, LD, b, b, b,
+                  GEMM_EPI_STORE, 0, st));
+  g_launches += 9;
+  QRB_CUDA_TRY(cudaMemcpyAsync(ws.hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  QRB_CUDA_TRY(cudaStreamSynchronize(st));
+  ++g_cholqr_panels;
+  if (*ws.hflag != 0) {
+    ++g_cholqr_fallbacks;
+    return QRB_OK;
+  }
+  // V below the top block: L2 = Q1[b:] R2^-1 Uc^-1 = Q1[b:] M, written over P[b:]
+  if (m > b)
+    QRB_TRY(gemm_nn(MatView{Wq + b, m - b, b, mw}, MatView{M, b, b, LD}, panel.ptr + b, panel.ld,
+                    m - b, b, b, GEMM_EPI_STORE, 0, st));
+  QRB_TRY(cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(T, sizeof(double) * ldt, Tt, sizeof(double) * LD,
+                                 sizeof(double) * b, b, cudaMemcpyDeviceToDevice, st));
+  g_launches += 3;
+  *done = true;
+  return QRB_OK;
+}
+
+static bool cholqr_eligible(const MatView& panel) {
+  if (g_panel_algo == 1) return false;
+  const int64_t m = panel.rows, b = panel.cols;
+  if (b < 2 || b > 128 || (b & 1) || m < b) return false;
+  if ((panel.ld & 1) || (reinterpret_cast<uintptr_t>(panel.ptr) & 15)) return false;
+  if (g_panel_algo == 2) return true;
+  return m >= g_cholqr_min_rows;
+}
+
 static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64_t ldt,
                              Workspace& ws, cudaStream_t st) {
   const int m = static_cast<int>(panel.rows);
@@ -209,6 +314,11 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
   if (m < pw) {
     set_last_error("panel rows < width");
     return QRB_ERR_ARG;
+  }
+  if (cholqr_eligible(panel)) {
+    bool done = false;
+    QRB_TRY(factor_panel_cholqr2(panel, tau, T, ldt, ws, st, &done));
+    if (done) return QRB_OK;
   }
   const int ldg = 128;
   QRB_TRY(ws.G.ensure(sizeof(double) * ldg * 128, st));
@@ -879,5 +989,36 @@ int qrb_release_workspace(void) {
 }
 
 int64_t qrb_launch_count(void) { return g_launches.load(); }
+
+int qrb_set_tuning(const char* key, int64_t value) {
+  const std::string k = key ? key : "";
+  if (k == "panel_algo" && value >= 0 && value <= 2) {
+    g_panel_algo = static_cast<int>(value);
+    return QRB_OK;
+  }
+  if (k == "cholqr_min_rows" && value >= 0) {
+    g_cholqr_min_rows = value;
+    return QRB_OK;
+  }
+  set_last_error("qrb_set_tuning: unknown key or bad value: " + k);
+  return QRB_ERR_ARG;
+}
+
+int qrb_get_tuning(const char* key, int64_t* value) {
+  const std::string k = key ? key : "";
+  if (!value) {
+    set_last_error("qrb_get_tuning: null value");
+    return QRB_ERR_ARG;
+  }
+  if (k == "panel_algo") *value = g_panel_algo;
+  else if (k == "cholqr_min_rows") *value = g_cholqr_min_rows;
+  else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
+  else if (k == "cholqr_fallbacks") *value = g_cholqr_fallbacks.load();
+  else {
+    set_last_error("qrb_get_tuning: unknown key: " + k);
+    return QRB_ERR_ARG;
+  }
+  return QRB_OK;
+}
 
 }  // extern "C"
