@@ -29,227 +29,297 @@ namespace qrb {
 
 namespace {
 
-constexpr int SD_THREADS = 1024;
+// One CTA of 512 threads per b x b (b <= 128) problem, always padded to 128
+// (identity / zero padding that factors trivially), so no thread tests b inside
+// a sweep.  Thread t owns column c = t % 128, rows i = g + 4q (g = t / 128,
+// q = 0..31) of the working matrix in REGISTERS for a whole sweep.  Each step
+// is one barrier: the row the next step needs (and for the LU the column) is
+// published to double-buffered shared vectors by the threads that finish it;
+// the multiplier vector is published already masked (zero for rows that must
+// not change), so the update is the same predicate-free
+//     x[q] -= m[g + 4q] * f_c
+// for every thread, 8 rows per chunk, chunks skipped warp-uniformly once all
+// their rows are finished.
+constexpr int SD_THREADS = 512;
+constexpr int NP = 128;
 
-__device__ __forceinline__ double warp_sum(double v) {
+struct SdBuf {
+  double row[2][NP];   // row k of the working matrix (f operands)
+  double mul[2][NP];   // masked multipliers
+  double piv[NP];
+  double rec[NP];
+  double sg[NP];
+  double red[SD_THREADS / 32];
+  int bad;
+};
+
+// x[q] -= m[g + 4q] * f for the chunks that contain a row > lo
+__device__ __forceinline__ void sweep_update(double (&x)[32], const double* m, int g, int lo,
+                                             double f) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int qc = 0; qc < 32; qc += 8) {
+    if (g + 4 * (qc + 7) > lo) {
+      double mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[qc + u] -= mv[u] * f;
+    }
+  }
+}
+
+// same, for the chunks that contain a row < hi
+__device__ __forceinline__ void sweep_update_below(double (&x)[32], const double* m, int g, int hi,
+                                                   double f) {
+#pragma unroll
+  for (int qc = 0; qc < 32; qc += 8) {
+    if (g + 4 * qc < hi) {
+      double mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[qc + u] -= mv[u] * f;
+    }
+  }
+}
+
+// value of row r (r % 4 == g) of this thread's column
+__device__ __forceinline__ double row_of(const double (&x)[32], int r) {
+  const int qr = r >> 2;
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q == qr) v = x[q];
   return v;
 }
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
-    v = warp_sum(v);
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  const double r = red[0];
-  __syncthreads();
-  return r;
+__device__ __forceinline__ void set_row(double (&x)[32], int r, double v) {
+  const int qr = r >> 2;
+#pragma unroll
+  for (int q = 0; q < 32; ++q)
+    if (q == qr) x[q] = v;
 }
 
-// In-place inverse of the upper triangle of a (ld L): X = U^-1 with X[r][c]
-// (r < c) stored transposed at a[c + r*L] (strictly lower part) and X[c][c] in
-// xd[c].  Row-oriented back substitution, 8 threads per column, one barrier
-// per row.
-__device__ void inv_upper_into_lower(double* a, int L, int b, double* xd) {
-  const int tid = threadIdx.x;
-  const int jj = tid >> 3, part = tid & 7;
-  for (int i = b - 1; i >= 0; --i) {
-    const int j = i + 1 + jj;
-    double s = 0.0;
-    if (j < b) {
-      for (int l = i + 1 + part; l <= j; l += 8)
-        s += a[i + l * L] * (l == j ? xd[j] : a[j + l * L]);
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    const double xii = 1.0 / a[i + i * L];
-    if (part == 0 && j < b) a[j + i * L] = -xii * s;
-    if (tid == 0) xd[i] = xii;
-    __syncthreads();
-  }
-}
-
-// In-place inverse of the unit lower triangle of a: Y = L^-1 (unit lower) with
-// Y[r][c] (r > c) stored transposed at a[c + r*L] (strictly upper part), i.e.
-// the strict upper part then holds L^-T.  Forward, one barrier per row.
-__device__ void inv_unit_lower_into_upper(double* a, int L, int b) {
-  const int tid = threadIdx.x;
-  const int jj = tid >> 3, part = tid & 7;
-  for (int i = 1; i < b; ++i) {
-    const int j = jj;  // Y[i][j], j < i
-    double s = 0.0;
-    if (j < i) {
-      // Y[i][j] = -sum_{l=j}^{i-1} L[i][l] Y[l][j],  Y[j][j] = 1
-      for (int l = j + part; l < i; l += 8) s += a[i + l * L] * (l == j ? 1.0 : a[j + l * L]);
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (part == 0 && j < i) a[j + i * L] = -s;
+// X = U^-1 (x[q] = X(g + 4q, c)) for U upper with unit-free diagonal in
+// sb.rec (reciprocals) and strictly upper part in shared memory u (ld lu,
+// diagonal and lower part stored as zero).  Bottom-up Gauss-Jordan: the
+// unscaled row k of X eliminates U(i, k) for i < k; its owners then scale it.
+__device__ void inv_upper_sweep(double (&x)[32], const double* u, int lu, SdBuf& sb) {
+  const int t = threadIdx.x, c = t & 127, g = t >> 7;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) x[q] = (g + 4 * q == c) ? 1.0 : 0.0;
+  sb.row[(NP - 1) & 1][c] = (c == NP - 1) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int k = NP - 1; k >= 0; --k) {
+    const double rk = sb.rec[k];
+    const double f = sb.row[k & 1][c] * rk;  // X(k, c) = 0 for c < k
+    sweep_update_below(x, u + (size_t)k * lu, g, k, f);  // U(i, k), zero for i >= k
+    if (g == (k & 3)) set_row(x, k, row_of(x, k) * rk);
+    if (k >= 1 && g == ((k - 1) & 3)) sb.row[(k - 1) & 1][c] = row_of(x, k - 1);
     __syncthreads();
   }
 }
 
 // R = chol(G) (upper, G = R^T R) and R^-1, both written b x b with zero lower part.
+// One sweep of symmetric Gaussian elimination on the full G; the row operations
+// applied to B = I give B = L^-1 of G = L D L^T, so R = D^-1/2 S and
+// R^-T = D^-1/2 L^-1.  Column c keeps S(i, c) for i <= c; below the diagonal
+// it holds the symmetric Schur complement until step c, when it turns into
+// B(i, c) = -S(i, c) / d_c, and is then updated as B with the same formula.
 __global__ void __launch_bounds__(SD_THREADS, 1)
     chol_inv_kernel(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, int* flag,
                     int bit, int check_identity) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
-  __shared__ int bad;
-  const int L = b + 1;
-  double* a = sm;
-  double* xd = a + (size_t)b * L;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
+  __shared__ SdBuf sb;
+  const int t = threadIdx.x, c = t & 127, g = t >> 7, lane = t & 31, warp = t >> 5;
+  double x[32];
+  if (t == 0) sb.bad = 0;
   double fro = 0.0;
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    if (r <= c) {
-      const double v = G[r + (int64_t)c * ldg];
-      a[r + c * L] = v;
-      const double d = v - (r == c ? 1.0 : 0.0);
-      fro += (r == c ? 1.0 : 2.0) * d * d;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int i = g + 4 * q;
+    double v = (i == c) ? 1.0 : 0.0;
+    if (i < b && c < b) {
+      v = G[min(i, c) + (int64_t)max(i, c) * ldg];  // upper triangle, mirrored
+      const double e = v - (i == c ? 1.0 : 0.0);
+      fro += e * e;
     }
+    x[q] = v;
   }
-  fro = block_sum(fro, red);  // includes a barrier
-  if (tid == 0 && (check_identity && !(fro <= 0.25))) bad = 1;
-  // right-looking Cholesky on the upper triangle; column j = tid % 128, rows i = g (mod 8)
-  const int j = tid & 127, g = tid >> 7;
-  for (int k = 0; k < b; ++k) {
-    double d = a[k + k * L];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if (lane == 0) sb.red[warp] = fro;
+  if (g == 0) {
+    sb.row[0][c] = x[0];
+    sb.mul[0][c] = c > 0 ? x[0] : 0.0;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < SD_THREADS / 32; ++w) tot += sb.red[w];
+    if (check_identity && !(tot <= 0.25)) sb.bad = 1;
+    double d = sb.row[0][0];
     if (!(d > 0.0 && d < INFINITY)) {
+      sb.bad = 1;
       d = 1.0;
-      if (tid == 0) bad = 1;
     }
-    if (j > k && j < b) {
-      const double akj = a[k + j * L] / d;
-      const int i0 = k + 1 + ((g - (k + 1)) & 7);
-      for (int i = i0; i <= j; i += 8) a[i + j * L] -= a[k + i * L] * akj;
+    sb.piv[0] = d;
+    sb.rec[0] = 1.0 / d;
+  }
+  __syncthreads();
+  for (int k = 0; k < NP; ++k) {
+    const double rk = sb.rec[k];
+    if (c != k) {
+      sweep_update(x, sb.mul[k & 1], g, k, sb.row[k & 1][c] * rk);
+    } else {
+      // column k: below the diagonal S(i, k) -> B(i, k) = -S(i, k) / d_k
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (g + 4 * q > k) x[q] *= -rk;
+    }
+    if (k + 1 < NP && g == ((k + 1) & 3)) {
+      const double v = row_of(x, k + 1);
+      sb.row[(k + 1) & 1][c] = v;
+      sb.mul[(k + 1) & 1][c] = c > k + 1 ? v : 0.0;
+      if (c == k + 1) {
+        double d = v;
+        if (!(d > 0.0 && d < INFINITY)) {
+          sb.bad = 1;
+          d = 1.0;
+        }
+        sb.piv[c] = d;
+        sb.rec[c] = 1.0 / d;
+      }
     }
     __syncthreads();
   }
-  // scale rows: R[k][c] = S[k][c] / sqrt(S[k][k])
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    if (r < c) {
-      double d = a[r + r * L];
-      if (!(d > 0.0 && d < INFINITY)) d = 1.0;
-      a[r + c * L] = a[r + c * L] / sqrt(d);
+  for (int r = t; r < NP; r += SD_THREADS) sb.rec[r] = 1.0 / sqrt(sb.piv[r]);
+  __syncthreads();
+  if (c < b) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int i = g + 4 * q;
+      if (i < b) {
+        if (i <= c) {
+          const double rv = x[q] * sb.rec[i];                  // R(i, c)
+          R[i + (int64_t)c * ldo] = rv;
+          if (i == c) Rinv[i + (int64_t)c * ldo] = sb.rec[c];  // (i < c) comes from column i
+          if (!(fabs(rv) < INFINITY)) sb.bad = 1;
+        } else {
+          const double xt = x[q] * sb.rec[i];                  // R^-1(c, i) = B(i, c)/sqrt(d_i)
+          R[i + (int64_t)c * ldo] = 0.0;
+          Rinv[i + (int64_t)c * ldo] = 0.0;
+          Rinv[c + (int64_t)i * ldo] = xt;
+          if (!(fabs(xt) < INFINITY)) sb.bad = 1;
+        }
+      }
     }
   }
   __syncthreads();
-  for (int r = tid; r < b; r += SD_THREADS) {
-    double d = a[r + r * L];
-    if (!(d > 0.0 && d < INFINITY)) d = 1.0;
-    a[r + r * L] = sqrt(d);
-  }
-  __syncthreads();
-  inv_upper_into_lower(a, L, b, xd);
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    const double rv = r <= c ? a[r + c * L] : 0.0;
-    const double xv = r < c ? a[c + r * L] : (r == c ? xd[c] : 0.0);
-    R[r + (int64_t)c * ldo] = rv;
-    Rinv[r + (int64_t)c * ldo] = xv;
-    if (!(fabs(xv) < INFINITY)) bad = 1;  // benign race: any writer sets 1
-  }
-  __syncthreads();
-  if (tid == 0 && bad) atomicOr(flag, bit);
+  if (t == 0 && sb.bad) atomicOr(flag, bit);
 }
 
-// Modified LU of Qt - S (Qt b x b, s chosen on the fly), then
-//   Uc (upper), NUcS = -Uc S, L1 (strict lower), Ucinv = Uc^-1, L1invT = L1^-T (unit upper), s.
+// Modified LU of Qt - diag(s) (s_k = -sign of the current pivot entry), then
+//   Uc (upper), NUcS = -Uc diag(s), L1 (strict lower), Ucinv = Uc^-1,
+//   L1invT = L1^-T (unit upper), s.
 __global__ void __launch_bounds__(SD_THREADS, 1)
     mlu_kernel(const double* Qt, int ldq, int b, double* Uc, double* NUcS, double* L1,
                double* Ucinv, double* L1invT, double* s_out, int ldo, int* flag, int bit) {
-  extern __shared__ double sm[];
-  __shared__ int bad;
-  const int L = b + 1;
-  double* a = sm;
-  double* xd = a + (size_t)b * L;
-  double* piv = xd + b;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    a[r + c * L] = Qt[r + (int64_t)c * ldq];
+  extern __shared__ double um[];  // NP x NP, ld NP + 1: strict upper of U, later of L1^T
+  __shared__ SdBuf sb;
+  const int t = threadIdx.x, c = t & 127, g = t >> 7;
+  constexpr int LU = NP + 1;
+  double x[32];
+  if (t == 0) sb.bad = 0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int i = g + 4 * q;
+    x[q] = (c < b && i < b) ? Qt[i + (int64_t)c * ldq] : 0.0;
+  }
+  auto pivot = [&](int k, double w) {
+    const double sgn = w >= 0.0 ? 1.0 : -1.0;
+    const double p = w + sgn;
+    sb.sg[k] = -sgn;
+    sb.piv[k] = p;
+    sb.rec[k] = 1.0 / p;
+    if (!(fabs(w) < INFINITY)) sb.bad = 1;
+  };
+  // row 0 (f operands), column 0 (masked multipliers), pivot 0
+  if (g == 0) sb.row[0][c] = x[0];
+  if (c == 0) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) sb.mul[0][g + 4 * q] = (g + 4 * q > 0) ? x[q] : 0.0;
+    if (g == 0) pivot(0, x[0]);
   }
   __syncthreads();
-  const int j = tid & 127, g = tid >> 7;
-  for (int k = 0; k < b; ++k) {
-    const double w = a[k + k * L];
-    const double p = w + (w >= 0.0 ? 1.0 : -1.0);  // w - s_k, s_k = -sign(w)
-    if (j > k && j < b) {
-      const double ukj = a[k + j * L] / p;
-      const int i0 = k + 1 + ((g - (k + 1)) & 7);
-      for (int i = i0; i < b; i += 8) a[i + j * L] -= a[i + k * L] * ukj;
+  for (int k = 0; k < NP; ++k) {
+    const double rk = sb.rec[k];
+    if (c > k) {
+      sweep_update(x, sb.mul[k & 1], g, k, sb.row[k & 1][c] * rk);  // A(i,c) -= A(i,k)/p_k A(k,c)
+    } else if (c == k) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (g + 4 * q > k) x[q] *= rk;  // column k becomes L(:, k)
+      if (g == (k & 3)) set_row(x, k, sb.piv[k]);
+    }
+    if (k + 1 < NP) {
+      if (g == ((k + 1) & 3) && c > k) sb.row[(k + 1) & 1][c] = row_of(x, k + 1);
+      if (c == k + 1) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) sb.mul[(k + 1) & 1][g + 4 * q] = (g + 4 * q > k + 1) ? x[q] : 0.0;
+        if (g == ((k + 1) & 3)) pivot(k + 1, row_of(x, k + 1));
+      }
     }
     __syncthreads();
   }
-  for (int k = tid; k < b; k += SD_THREADS) {
-    const double w = a[k + k * L];
-    const double sg = w >= 0.0 ? 1.0 : -1.0;
-    piv[k] = w + sg;
-    s_out[k] = -sg;
-    if (!(fabs(w) < INFINITY)) bad = 1;
-  }
-  __syncthreads();
-  // L1[i][k] = a[i][k] / piv_k ; Uc[k][c] = a[k][c] (c > k), Uc[k][k] = piv_k
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    double u = 0.0, l = 0.0;
-    if (r > c) {
-      l = a[r + c * L] / piv[c];
-      a[r + c * L] = l;
-    } else if (r == c) {
-      u = piv[c];
-      a[r + c * L] = u;
-    } else {
-      u = a[r + c * L];
+  // outputs Uc, NUcS, L1, s; strict upper of U into shared memory, 1/U(k,k) into rec
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int i = g + 4 * q;
+    const double v = x[q];
+    if (c < b && i < b) {
+      Uc[i + (int64_t)c * ldo] = i <= c ? v : 0.0;
+      NUcS[i + (int64_t)c * ldo] = i <= c ? -v * sb.sg[c] : 0.0;
+      L1[i + (int64_t)c * ldo] = i > c ? v : 0.0;
+      if (!(fabs(v) < INFINITY)) sb.bad = 1;
     }
-    Uc[r + (int64_t)c * ldo] = u;
-    L1[r + (int64_t)c * ldo] = l;
+    um[i + (size_t)c * LU] = i < c ? v : 0.0;
+  }
+  if (t < NP) {
+    if (t < b) s_out[t] = sb.sg[t];
+    sb.rec[t] = 1.0 / sb.piv[t];
   }
   __syncthreads();
-  // NUcS = -Uc diag(s): column c scaled by -s_c
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    NUcS[r + (int64_t)c * ldo] = r <= c ? -a[r + c * L] * s_out[c] : 0.0;
+  inv_upper_sweep(x, um, LU, sb);
+  if (c < b) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int i = g + 4 * q;
+      if (i < b) {
+        Ucinv[i + (int64_t)c * ldo] = i <= c ? x[q] : 0.0;
+        if (!(fabs(x[q]) < INFINITY)) sb.bad = 1;
+      }
+    }
   }
   __syncthreads();
-  // Uc^-1 into the strict lower part (L1 saved to global above)
-  inv_upper_into_lower(a, L, b, xd);
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    const double xv = r < c ? a[c + r * L] : (r == c ? xd[c] : 0.0);
-    Ucinv[r + (int64_t)c * ldo] = xv;
-    if (!(fabs(xv) < INFINITY)) bad = 1;
+  // L1^T (strict upper; L1 re-read from global memory, written by this CTA above)
+  for (int idx = t; idx < NP * NP; idx += SD_THREADS) {
+    const int cc = idx / NP, r = idx - cc * NP;
+    um[r + (size_t)cc * LU] = (r < cc && cc < b) ? L1[cc + (int64_t)r * ldo] : 0.0;
+  }
+  if (t < NP) sb.rec[t] = 1.0;
+  __syncthreads();
+  inv_upper_sweep(x, um, LU, sb);
+  if (c < b) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int i = g + 4 * q;
+      if (i < b) {
+        L1invT[i + (int64_t)c * ldo] = i <= c ? x[q] : 0.0;
+        if (!(fabs(x[q]) < INFINITY)) sb.bad = 1;
+      }
+    }
   }
   __syncthreads();
-  // reload L1 into the strict lower part, invert into the strict upper part
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    if (r > c) a[r + c * L] = L1[r + (int64_t)c * ldo];
-  }
-  __syncthreads();
-  inv_unit_lower_into_upper(a, L, b);
-  for (int idx = tid; idx < b * b; idx += SD_THREADS) {
-    const int c = idx / b, r = idx - c * b;
-    const double v = r < c ? a[r + c * L] : (r == c ? 1.0 : 0.0);
-    L1invT[r + (int64_t)c * ldo] = v;
-    if (!(fabs(v) < INFINITY)) bad = 1;
-  }
-  __syncthreads();
-  if (tid == 0 && bad) atomicOr(flag, bit);
+  if (t == 0 && sb.bad) atomicOr(flag, bit);
 }
 
 // P[0:b, 0:b] <- S R (on/above the diagonal) and L1 (below); tau_k = T_kk
@@ -263,7 +333,7 @@ __global__ void cholqr_write_top_kernel(double* P, int64_t ldp, int b, const dou
   if (r == c) tau[c] = T[c + c * ldt];
 }
 
-size_t sd_smem(int b) { return ((size_t)b * (b + 1) + 2 * (size_t)b + 8) * sizeof(double); }
+size_t sd_smem(int) { return (size_t)NP * (NP + 1) * sizeof(double); }
 
 }  // namespace
 
@@ -275,11 +345,9 @@ int chol_inv(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, 
   }
   static bool configured = false;
   if (!configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sd_smem(128)));
     configured = true;
   }
-  chol_inv_kernel<<<1, SD_THREADS, sd_smem(b), stream>>>(G, ldg, b, R, Rinv, ldo, flag, bit,
+  chol_inv_kernel<<<1, SD_THREADS, 0, stream>>>(G, ldg, b, R, Rinv, ldo, flag, bit,
                                                           check_identity);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
