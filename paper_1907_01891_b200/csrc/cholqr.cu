@@ -63,7 +63,7 @@ __device__ __forceinline__ void sweep_update(double (&x)[32], const double* m, i
 #pragma unroll
       for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[qc + u] -= mv[u] * f;
+      for (int u = 0; u < 8; ++u) x[qc + u] = __fma_rn(-mv[u], f, x[qc + u]);
     }
   }
 }
@@ -78,7 +78,7 @@ __device__ __forceinline__ void sweep_update_below(double (&x)[32], const double
 #pragma unroll
       for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[qc + u] -= mv[u] * f;
+      for (int u = 0; u < 8; ++u) x[qc + u] = __fma_rn(-mv[u], f, x[qc + u]);
     }
   }
 }
@@ -112,9 +112,11 @@ __device__ void inv_upper_sweep(double (&x)[32], const double* u, int lu, SdBuf&
   for (int k = NP - 1; k >= 0; --k) {
     const double rk = sb.rec[k];
     const double f = sb.row[k & 1][c] * rk;  // X(k, c) = 0 for c < k
+    // row k-1 for the next step first (same fma as the chunk update below)
+    if (k >= 1 && g == ((k - 1) & 3))
+      sb.row[(k - 1) & 1][c] = __fma_rn(-u[(k - 1) + (size_t)k * lu], f, row_of(x, k - 1));
     sweep_update_below(x, u + (size_t)k * lu, g, k, f);  // U(i, k), zero for i >= k
     if (g == (k & 3)) set_row(x, k, row_of(x, k) * rk);
-    if (k >= 1 && g == ((k - 1) & 3)) sb.row[(k - 1) & 1][c] = row_of(x, k - 1);
     __syncthreads();
   }
 }
@@ -167,16 +169,12 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   __syncthreads();
   for (int k = 0; k < NP; ++k) {
     const double rk = sb.rec[k];
-    if (c != k) {
-      sweep_update(x, sb.mul[k & 1], g, k, sb.row[k & 1][c] * rk);
-    } else {
-      // column k: below the diagonal S(i, k) -> B(i, k) = -S(i, k) / d_k
-#pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (g + 4 * q > k) x[q] *= -rk;
-    }
+    const double* mul = sb.mul[k & 1];
+    const double f = sb.row[k & 1][c] * rk;
+    // row k+1 and pivot k+1 for the next step first (same arithmetic as below)
     if (k + 1 < NP && g == ((k + 1) & 3)) {
-      const double v = row_of(x, k + 1);
+      double v = row_of(x, k + 1);
+      v = c != k ? __fma_rn(-mul[k + 1], f, v) : v * -rk;
       sb.row[(k + 1) & 1][c] = v;
       sb.mul[(k + 1) & 1][c] = c > k + 1 ? v : 0.0;
       if (c == k + 1) {
@@ -188,6 +186,14 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
         sb.piv[c] = d;
         sb.rec[c] = 1.0 / d;
       }
+    }
+    if (c != k) {
+      sweep_update(x, mul, g, k, f);
+    } else {
+      // column k: below the diagonal S(i, k) -> B(i, k) = -S(i, k) / d_k
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (g + 4 * q > k) x[q] *= -rk;
     }
     __syncthreads();
   }
@@ -217,16 +223,13 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   if (t == 0 && sb.bad) atomicOr(flag, bit);
 }
 
-// Modified LU of Qt - diag(s) (s_k = -sign of the current pivot entry), then
-//   Uc (upper), NUcS = -Uc diag(s), L1 (strict lower), Ucinv = Uc^-1,
-//   L1invT = L1^-T (unit upper), s.
+// Modified LU of Qt - diag(s) (s_k = -sign of the current pivot entry):
+//   Uc (upper), NUcS = -Uc diag(s), L1 (strict lower), s.
 __global__ void __launch_bounds__(SD_THREADS, 1)
     mlu_kernel(const double* Qt, int ldq, int b, double* Uc, double* NUcS, double* L1,
-               double* Ucinv, double* L1invT, double* s_out, int ldo, int* flag, int bit) {
-  extern __shared__ double um[];  // NP x NP, ld NP + 1: strict upper of U, later of L1^T
+               double* s_out, int ldo, int* flag, int bit) {
   __shared__ SdBuf sb;
   const int t = threadIdx.x, c = t & 127, g = t >> 7;
-  constexpr int LU = NP + 1;
   double x[32];
   if (t == 0) sb.bad = 0;
 #pragma unroll
@@ -252,25 +255,28 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   __syncthreads();
   for (int k = 0; k < NP; ++k) {
     const double rk = sb.rec[k];
+    const double* mul = sb.mul[k & 1];
+    const double f = c > k ? sb.row[k & 1][c] * rk : 0.0;
+    // row k+1 and pivot k+1 for the next step first (same arithmetic as below)
+    if (k + 1 < NP && g == ((k + 1) & 3) && c > k) {
+      const double v = __fma_rn(-mul[k + 1], f, row_of(x, k + 1));
+      sb.row[(k + 1) & 1][c] = v;
+      if (c == k + 1) pivot(k + 1, v);
+    }
     if (c > k) {
-      sweep_update(x, sb.mul[k & 1], g, k, sb.row[k & 1][c] * rk);  // A(i,c) -= A(i,k)/p_k A(k,c)
+      sweep_update(x, mul, g, k, f);  // A(i,c) -= A(i,k)/p_k A(k,c)
+      if (c == k + 1) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) sb.mul[(k + 1) & 1][g + 4 * q] = (g + 4 * q > k + 1) ? x[q] : 0.0;
+      }
     } else if (c == k) {
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         if (g + 4 * q > k) x[q] *= rk;  // column k becomes L(:, k)
       if (g == (k & 3)) set_row(x, k, sb.piv[k]);
     }
-    if (k + 1 < NP) {
-      if (g == ((k + 1) & 3) && c > k) sb.row[(k + 1) & 1][c] = row_of(x, k + 1);
-      if (c == k + 1) {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) sb.mul[(k + 1) & 1][g + 4 * q] = (g + 4 * q > k + 1) ? x[q] : 0.0;
-        if (g == ((k + 1) & 3)) pivot(k + 1, row_of(x, k + 1));
-      }
-    }
     __syncthreads();
   }
-  // outputs Uc, NUcS, L1, s; strict upper of U into shared memory, 1/U(k,k) into rec
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
     const int i = g + 4 * q;
@@ -281,39 +287,40 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
       L1[i + (int64_t)c * ldo] = i > c ? v : 0.0;
       if (!(fabs(v) < INFINITY)) sb.bad = 1;
     }
-    um[i + (size_t)c * LU] = i < c ? v : 0.0;
   }
-  if (t < NP) {
-    if (t < b) s_out[t] = sb.sg[t];
-    sb.rec[t] = 1.0 / sb.piv[t];
-  }
+  if (t < b) s_out[t] = sb.sg[t];
   __syncthreads();
-  inv_upper_sweep(x, um, LU, sb);
-  if (c < b) {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int i = g + 4 * q;
-      if (i < b) {
-        Ucinv[i + (int64_t)c * ldo] = i <= c ? x[q] : 0.0;
-        if (!(fabs(x[q]) < INFINITY)) sb.bad = 1;
-      }
-    }
-  }
-  __syncthreads();
-  // L1^T (strict upper; L1 re-read from global memory, written by this CTA above)
+  if (t == 0 && sb.bad) atomicOr(flag, bit);
+}
+
+// CTA 0: Ucinv = Uc^-1;  CTA 1: L1invT = (L1^T)^-1 (unit upper).  Padded to NP
+// with the identity.
+__global__ void __launch_bounds__(SD_THREADS, 1)
+    tri_inv_kernel(const double* Uc, const double* L1, int b, double* Ucinv, double* L1invT,
+                   int ldo, int* flag, int bit) {
+  extern __shared__ double um[];  // strict upper part, ld NP + 1
+  __shared__ SdBuf sb;
+  constexpr int LU = NP + 1;
+  const int t = threadIdx.x, c = t & 127, g = t >> 7;
+  const bool lower = blockIdx.x == 1;
+  if (t == 0) sb.bad = 0;
   for (int idx = t; idx < NP * NP; idx += SD_THREADS) {
     const int cc = idx / NP, r = idx - cc * NP;
-    um[r + (size_t)cc * LU] = (r < cc && cc < b) ? L1[cc + (int64_t)r * ldo] : 0.0;
+    double v = 0.0;
+    if (r < cc && cc < b) v = lower ? L1[cc + (int64_t)r * ldo] : Uc[r + (int64_t)cc * ldo];
+    um[r + (size_t)cc * LU] = v;
   }
-  if (t < NP) sb.rec[t] = 1.0;
+  if (t < NP) sb.rec[t] = (lower || t >= b) ? 1.0 : 1.0 / Uc[t + (int64_t)t * ldo];
   __syncthreads();
+  double x[32];
   inv_upper_sweep(x, um, LU, sb);
+  double* out = lower ? L1invT : Ucinv;
   if (c < b) {
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
       const int i = g + 4 * q;
       if (i < b) {
-        L1invT[i + (int64_t)c * ldo] = i <= c ? x[q] : 0.0;
+        out[i + (int64_t)c * ldo] = i <= c ? x[q] : 0.0;
         if (!(fabs(x[q]) < INFINITY)) sb.bad = 1;
       }
     }
@@ -362,12 +369,13 @@ int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, doub
   }
   static bool configured = false;
   if (!configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(mlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QRB_CUDA_TRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sd_smem(128)));
     configured = true;
   }
-  mlu_kernel<<<1, SD_THREADS, sd_smem(b), stream>>>(Qt, ldq, b, Uc, NUcS, L1, Ucinv, L1invT, s,
-                                                     ldo, flag, bit);
+  mlu_kernel<<<1, SD_THREADS, 0, stream>>>(Qt, ldq, b, Uc, NUcS, L1, s, ldo, flag, bit);
+  QRB_CUDA_TRY(cudaGetLastError());
+  tri_inv_kernel<<<2, SD_THREADS, sd_smem(b), stream>>>(Uc, L1, b, Ucinv, L1invT, ldo, flag, bit);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
 }

@@ -216,7 +216,7 @@ static int g_panel_algo = [] {
   const char* e = std::getenv("QRB_PANEL_ALGO");
   return e ? std::atoi(e) : 0;
 }();
-static int64_t g_cholqr_min_rows = 4096;
+static int64_t g_cholqr_min_rows = 32768;  // measured crossover vs the Householder panel (r01)
 static std::atomic<int64_t> g_cholqr_panels{0}, g_cholqr_fallbacks{0};
 
 // CholeskyQR2 + Householder reconstruction of an m x b panel (cholqr.cu header
@@ -277,7 +277,7 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
                   st));
   QRB_TRY(gemm_nn(MatView{NUcS, b, b, LD}, MatView{L1iT, b, b, LD}, Tt, LD, b, b, b,
                   GEMM_EPI_STORE, 0, st));
-  g_launches += 9;
+  g_launches += 10;
   QRB_CUDA_TRY(cudaMemcpyAsync(ws.hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   QRB_CUDA_TRY(cudaStreamSynchronize(st));
   ++g_cholqr_panels;
