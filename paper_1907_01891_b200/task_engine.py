@@ -47,9 +47,12 @@ class EngineConfig:
 
     ``tile_size`` / ``inner_block`` keep their reference meaning for the
     on-disk stores and the API checks; ``panel_width`` is the GPU panel width
-    nb (a multiple of 16, <= 128) and ``device`` the CUDA device.  The disk
-    cache knobs are accepted and validated but unused: the matrix is resident
-    in HBM.
+    nb (a multiple of 16, <= 128) and ``device`` the CUDA device.  Residency
+    tiers: a matrix that fits ``hbm_budget_bytes`` is factored in HBM; one that
+    does not but fits ``cache_budget_bytes`` (the reference's RAM budget) is
+    pinned in host memory and streamed super-panel by super-panel (ooc.py);
+    anything larger streams panel by panel from the tile files on disk
+    (disk_ooc.py), the reference's own out-of-core regime.
     """
 
     tile_size: int = 10240
@@ -282,6 +285,42 @@ def _fits_in_hbm(rows: int, cols: int, cfg: EngineConfig) -> bool:
     return 8 * lda * cols + (1 << 30) <= _hbm_budget(cfg)
 
 
+def _fits_in_host(rows: int, cols: int, cfg: EngineConfig) -> bool:
+    lda = (rows + 31) // 32 * 32
+    return 8 * lda * cols <= cfg.cache_budget_bytes
+
+
+def _factorize_disk_staged(a: TiledMatrix, cfg: EngineConfig, factors_dir: Path,
+                           geometry_hash: str) -> tuple["QrFactors", RunReport]:
+    from .disk_ooc import DiskStagedQR
+    t_start = time.perf_counter()
+    b = a.tile_size
+    factored = TiledMatrix.create(a.rows, a.cols, b, factors_dir / "factored")
+    q = DiskStagedQR(a, factored, nb=cfg.panel_width, budget_bytes=_hbm_budget(cfg),
+                     io_threads=max(1, cfg.io_agents) + 1)
+    try:
+        st = q.factorize()
+    except (OSError, CorruptTileError) as exc:
+        q.close()
+        raise TaskIoError(0, "disk_staged_factorize", exc) from exc
+    factors = QrFactors(factored=factored, inner_block=cfg.inner_block, rows=a.rows,
+                        cols=a.cols, tile_size=b, panel_width=cfg.panel_width,
+                        geometry_hash=geometry_hash, directory=factors_dir)
+    q.tau.cpu().numpy()[:a.cols].astype("<f8").tofile(factors_dir / _TAU_NAME)
+    q.t_all.cpu().numpy().T.astype("<f8").ravel(order="F").tofile(factors_dir / _T_NAME)
+    factors.save_meta(factors_dir)
+    factors.host_state = q
+    report = RunReport(
+        mode=cfg.mode, task_count=0, total_seconds=time.perf_counter() - t_start,
+        compute_seconds=st["seconds"], io_read_seconds=st["read_s"],
+        io_write_seconds=st["write_s"], tiles_read=0, tiles_written=a.grid_rows * a.grid_cols,
+        cache_hits=0,
+        trace=[TaskTrace(0, "qr_disk_staged_superpanels", st["seconds"] * 1e3,
+                         st["read_s"] * 1e3, st["write_s"] * 1e3)],
+        gpu_flops=2.0 * a.rows * a.cols ** 2 - 2.0 * a.cols ** 3 / 3.0, h2d_seconds=0.0)
+    return factors, report
+
+
 def _pinned_from_tiles(store: TiledMatrix, rows: int, cols: int):
     """(n, lda) pinned host tensor (column-major m x n) filled from a tile store."""
     import torch
@@ -349,7 +388,9 @@ def factorize(a: TiledMatrix, config: EngineConfig, factors_dir,
     factors_dir = Path(factors_dir)
     factors_dir.mkdir(parents=True, exist_ok=True)
     if not _fits_in_hbm(a.rows, a.cols, cfg):
-        return _factorize_host_staged(a, cfg, factors_dir, geometry_hash)
+        if _fits_in_host(a.rows, a.cols, cfg):
+            return _factorize_host_staged(a, cfg, factors_dir, geometry_hash)
+        return _factorize_disk_staged(a, cfg, factors_dir, geometry_hash)
     t_start = time.perf_counter()
     dev = QrDevice(a.rows, a.cols, cfg.panel_width, cfg.device)
     b = a.tile_size
@@ -452,9 +493,21 @@ def _solve_host_staged(factors: "QrFactors", b_mat: TiledMatrix, cfg: EngineConf
                        out_dir: Path) -> tuple[TiledMatrix, RunReport]:
     import torch
 
+    from .disk_ooc import DiskStagedQR
     from .ooc import HostStagedQR
     t_start = time.perf_counter()
     q = factors.host_state
+    if q is None and not _fits_in_host(factors.rows, factors.cols, cfg):
+        q = DiskStagedQR(None, factors.factored, nb=factors.panel_width,
+                         budget_bytes=_hbm_budget(cfg))
+        npan = -(-factors.cols // factors.panel_width)
+        nb = factors.panel_width
+        tau = np.fromfile(factors.directory / _TAU_NAME, dtype="<f8")
+        t = np.fromfile(factors.directory / _T_NAME, dtype="<f8").reshape((nb, npan * nb),
+                                                                          order="F")
+        q.tau[:factors.cols] = torch.from_numpy(tau).cuda()
+        q.t_all.copy_(torch.from_numpy(np.ascontiguousarray(t.T)).cuda())
+        factors.host_state = q
     if q is None:
         host = _pinned_from_tiles(factors.factored, factors.rows, factors.cols)
         q = HostStagedQR(host, factors.rows, factors.cols, nb=factors.panel_width,
