@@ -202,7 +202,8 @@ def ours_arm(args, rank: int, world: int):
     a_sample = a_dev[:min(CPU_SAMPLE_COLS, n), :m].cpu().numpy().T.copy()
     # sinograms b = A x + 1% noise (seeded per slice); A x via the device matrix
     xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()        # (S, n)
-    ax = (xt @ a_dev[:, :m]).cpu().numpy().T                            # (m, S)
+    ax_dev = xt @ a_dev[:, :m]                                           # (S, m), noiseless
+    ax = ax_dev.cpu().numpy().T                                          # (m, S)
     b_host = cs.noisy_sinograms(ax, args.config)
     ldb = lda
     b_dev = torch.zeros((S, ldb), dtype=torch.float64, device="cuda")
@@ -276,7 +277,18 @@ def ours_arm(args, rank: int, world: int):
                "ssim_avg": float(metrics.ssim(xt_dev, x_last.T, g.image_pixels).mean()),
                "relative_residual": metrics.relative_residual(a_dev, x_last.T, b_dev[:, :m].T, m),
                "note": "noisy sinograms (1% Gaussian), least-squares solution"}
-    del xt_dev
+    # the same slices from the noiseless sinograms A x_true: the least-squares
+    # solution must reproduce the phantoms (size-independent correctness check;
+    # the noisy numbers above measure the conditioning of A, not the solver)
+    b0 = torch.zeros_like(b_dev)
+    b0[:, :m] = ax_dev
+    x0 = torch.zeros_like(x_dev)
+    q.solve_device(b0, x0, None)
+    x0n = x0[:, :n]
+    err = torch.linalg.norm(x0n - xt_dev.T, dim=1) / torch.linalg.norm(xt_dev.T, dim=1)
+    quality["noiseless"] = {"psnr_avg_db": float(metrics.psnr(xt_dev, x0n.T, g.image_pixels).mean()),
+                            "x_rel_err_max": float(err.max())}
+    del xt_dev, b0, x0, ax_dev
 
     # config 5: solve throughput of a 4096-slice batch against the config-3 factors
     cfg5 = None
