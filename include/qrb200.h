@@ -124,6 +124,18 @@ QRB_API int qrb_set_profiling(qrb_handle* h, int on);
  * Returns QRB_ENONFINITE if A holds NaN/Inf (KernelInputError, kernels.py:305-306). */
 QRB_API int qrb_factorize(qrb_handle* h, qrb_report* rep);
 
+/* qrb_set_matrix(host) + qrb_factorize with the PCIe copy overlapped: A (host,
+ * column-major, leading dim ld; pinned memory for overlap) is copied in column
+ * chunks of `chunk_cols` (0 = automatic) on a copy stream, and each chunk is
+ * factored left-looking as soon as it lands -- all earlier panels applied to
+ * it, then its own panels -- the reference's left-looking order
+ * (task_engine.py:187-217) applied to host->HBM staging.  Same factors and
+ * flop count as qrb_factorize; rep->h2d_ms / h2d_bytes report the copy, and
+ * rep->total_ms runs from the first copy to the last panel.
+ * Replaces: factorize's stage-and-execute sequence (task_engine.py:606-641). */
+QRB_API int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
+                               qrb_report* rep);
+
 /* Persisted-factor interop: tau (n) and the per-panel T factors
  * (nb x nb each, panel k at T + k*nb*ldt... stored as an nb x (npanels*nb) matrix). */
 QRB_API int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt);

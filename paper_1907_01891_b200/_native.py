@@ -75,6 +75,7 @@ SIGNATURES = {
     "qrb_set_profiling": (c_int, [c_void_p, c_int]),
     "qrb_set_stream": (c_int, [c_void_p, c_void_p]),
     "qrb_factorize": (c_int, [c_void_p, ctypes.POINTER(QrbReport)]),
+    "qrb_factorize_host": (c_int, [c_void_p, c_void_p, c_i64, c_i64, ctypes.POINTER(QrbReport)]),
     "qrb_get_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_set_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_solve": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p, c_int,

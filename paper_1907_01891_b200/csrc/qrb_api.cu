@@ -709,6 +709,114 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   return QRB_OK;
 }
 
+int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
+                       qrb_report* rep) {
+  clear_report(rep);
+  if (!h || !src || ld < h->m || chunk_cols < 0) {
+    set_last_error("qrb_factorize_host: bad arguments");
+    return QRB_EARG;
+  }
+  DeviceGuard g(h->device);
+  Workspace& ws = device_workspace();
+  const int64_t launches0 = g_launches.load();
+  cudaStream_t st = h->stream;
+  const int nb = h->nb;
+  int64_t W = chunk_cols;
+  if (W == 0) W = std::max<int64_t>(8192, (h->n / 8 + nb - 1) / nb * nb);
+  W = std::max<int64_t>(nb, (W + nb - 1) / nb * nb);
+  const int64_t nchunks = (h->n + W - 1) / W;
+  cudaStream_t cs = nullptr;
+  QRB_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> landed(nchunks, nullptr);
+  cudaEvent_t c0ev = nullptr, c1ev = nullptr;
+  auto cleanup = [&]() {
+    for (auto& e : landed)
+      if (e) cudaEventDestroy(e);
+    if (c0ev) cudaEventDestroy(c0ev);
+    if (c1ev) cudaEventDestroy(c1ev);
+    if (cs) cudaStreamDestroy(cs);
+  };
+  int status = QRB_OK;
+  do {
+    if (cudaEventCreate(&c0ev) != cudaSuccess || cudaEventCreate(&c1ev) != cudaSuccess) {
+      status = QRB_ECUDA;
+      break;
+    }
+    // the copy stream starts after everything already queued on the handle's stream
+    cudaEventRecord(h->ev0, st);
+    cudaStreamWaitEvent(cs, h->ev0, 0);
+    cudaEventRecord(c0ev, cs);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
+      if (cudaEventCreateWithFlags(&landed[c], cudaEventDisableTiming) != cudaSuccess ||
+          cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double), src + col0 * ld,
+                            ld * sizeof(double), h->m * sizeof(double), nc,
+                            cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+          cudaEventRecord(landed[c], cs) != cudaSuccess) {
+        set_last_error(std::string("qrb_factorize_host: copy: ") +
+                       cudaGetErrorString(cudaGetLastError()));
+        status = QRB_ECUDA;
+        break;
+      }
+    }
+    if (status != QRB_OK) break;
+    cudaEventRecord(c1ev, cs);
+    ProfSession session(h);
+    MatView A{h->A, h->m, h->n, h->lda};
+    // non-finite input check per landed chunk (flag read once at the end)
+    QRB_TRY(ws.bar.ensure(64, st));
+    int* nf = static_cast<int*>(ws.bar.p) + 8;
+    QRB_CUDA_TRY(cudaMemsetAsync(nf, 0, sizeof(int), st));
+    for (int64_t c = 0; c < nchunks && status == QRB_OK; ++c) {
+      const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
+      QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[c], 0));
+      nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, nc, nf);
+      g_launches += 1;
+      // left-looking: every earlier panel applied to this chunk, in order
+      const int kc0 = static_cast<int>(col0 / nb);
+      for (int k = 0; k < kc0 && status == QRB_OK; ++k) {
+        const int64_t j0 = int64_t(k) * nb, mk = h->m - j0;
+        status = apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
+                          A.sub(j0, col0, mk, nc), ws, st);
+      }
+      // then the chunk's own panels, right-looking inside the chunk
+      for (int64_t j0 = col0; j0 < col0 + nc && status == QRB_OK; j0 += nb) {
+        const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
+        const int k = static_cast<int>(j0 / nb);
+        double* Tk = h->T + int64_t(k) * nb * nb;
+        status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
+        const int64_t rest = col0 + nc - (j0 + pw);
+        if (status == QRB_OK && rest > 0)
+          status = apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, rest), ws, st);
+      }
+    }
+    if (status != QRB_OK) break;
+    QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
+    QRB_CUDA_TRY(cudaEventSynchronize(h->ev1));
+    QRB_CUDA_TRY(cudaGetLastError());
+    session.finish(rep);
+    int hflag = 0;
+    QRB_CUDA_TRY(cudaMemcpy(&hflag, nf, sizeof(int), cudaMemcpyDeviceToHost));
+    h->factored = hflag == 0;
+    h->rinv_ready = false;
+    if (hflag) {
+      set_last_error("factorize: input matrix has non-finite entries");
+      status = QRB_ENONFINITE;
+      break;
+    }
+    if (rep) {
+      const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
+      rep->total_ms = elapsed(h->ev0, h->ev1);
+      rep->h2d_ms = elapsed(c0ev, c1ev);
+      rep->h2d_bytes = 8.0 * m * n;
+      rep->flops = 2.0 * m * n * n - 2.0 * n * n * n / 3.0;
+      rep->kernel_launches = g_launches.load() - launches0;
+    }
+  } while (false);
+  cleanup();
+  return status;
+}
+
 int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt) {
   if (!h || (T && ldt < h->nb)) return QRB_EARG;
   DeviceGuard g(h->device);

@@ -156,6 +156,19 @@ class QrDevice:
         self.last_report = rep.as_dict()
         return self.last_report
 
+    def factorize_host(self, a, chunk_cols: int = 0) -> dict:
+        """set_matrix(host A) + factorize with the PCIe copy overlapped: A is
+        copied in column chunks and each chunk is factored left-looking as soon
+        as it lands (qrb_factorize_host).  Pass pinned memory for real overlap."""
+        a, lda = _host_colmajor(a)
+        if a.shape != (self.m, self.n):
+            raise ValueError(f"matrix must be {self.m}x{self.n}, got {a.shape}")
+        rep = _native.QrbReport()
+        _native.check(self.lib.qrb_factorize_host(self._h, _ptr(a), lda, int(chunk_cols),
+                                                  ctypes.byref(rep)), "qrb_factorize_host")
+        self.last_report = rep.as_dict()
+        return self.last_report
+
     def solve(self, b, report_block: int | None = None, want_resid: bool = True, out=None):
         """X = R^-1 (Q^T B)[:n] for host B (m x nrhs); returns (X, resid, report).
         ``out`` may be a preallocated (n x nrhs) column-contiguous host array."""
