@@ -166,7 +166,7 @@ def reference_arm(args, rank: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Siddon fan-beam A, seeded)",
         "config": {"workload": f"config{args.config}: QR sample = leading {g.n_rays}x{ncol} "
                                f"column block of A", "m": g.n_rays, "n": ncol,
@@ -351,7 +351,7 @@ def ours_arm(args, rank: int, world: int):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Siddon fan-beam A from seeded geometry; seeded 10-ellipse phantoms, "
                 "1% Gaussian noise)",
         "config": {"workload": f"config{args.config}: QR of A {m}x{n} fp64 + solve {S} slices",
