@@ -176,7 +176,7 @@ def reference_arm(args, rank: int):
                                    f"({g.n_rays}x{ncol}), b=1024, w=128"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # -- our arm -----------------------------------------------------------------------------------
@@ -371,7 +371,25 @@ def ours_arm(args, rank: int, world: int):
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s, "densify_s": densify_s,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_FD: int | None = None
+
+
+def claim_stdout() -> None:
+    """Keep fd 1 for the one JSON line; anything native libraries write to fd 1
+    (e.g. the NCCL version banner) goes to stderr instead."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    sys.stdout.flush()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
 def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
@@ -414,6 +432,7 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()
+    claim_stdout()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":

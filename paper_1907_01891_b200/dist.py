@@ -173,6 +173,10 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
     la = lookahead and world > 1
     ops.sync()
     t0 = time.perf_counter()
+    ev = None
+    if a_local.is_cuda:                  # device time of the whole factorization
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
     if rank == owner_of(0, world):
         factor_and_pack(0)
     pending = start_bcast(0)
@@ -201,8 +205,13 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
             apply(k, lfirst, n_local)
             if not la and nxt < npan:
                 pending = start_bcast(nxt)
+    if ev is not None:
+        ev[1].record()
     ops.sync()
     secs = time.perf_counter() - t0
+    if ev is not None:
+        stats["wall_seconds"] = secs
+        secs = ev[0].elapsed_time(ev[1]) / 1e3
     return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats)
 
 
@@ -324,8 +333,8 @@ def bench_rank(args, rank: int, world: int):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", local_rank))
-    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload, qr_flops,
-                       solve_flops)
+    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload, emit,
+                       qr_flops, solve_flops)
     from . import ct_system as cs
     from .device import QrDevice, launch_count
 
@@ -451,6 +460,11 @@ def bench_rank(args, rank: int, world: int):
             "solve_path": "streamed V/R broadcast (no replication)" if lean else
                           "all-gathered factors, per-rank solve",
             "gpu_launches": int(launches), "clocks": clocks,
+            "roofline": {"bound": "tensor", "achieved": value / world,
+                         "peak": FP64_PEAK_TFLOPS, "unit": UNIT,
+                         "frac": value / world / FP64_PEAK_TFLOPS, "traffic": None,
+                         "kernel": "whole factorization per GPU (CUDA events, max over "
+                                   "ranks); per-kernel accounting is single-GPU only"},
             "e2e": {"value": fl / float(e2e_s) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * lda * n + 8 * m * S),
                     "d2h_bytes_per_step": int(8 * n * S),
@@ -459,5 +473,5 @@ def bench_rank(args, rank: int, world: int):
                             ("streamed V/R solve" if lean else "all-gather -> QrDevice.solve") +
                             " (host B share -> host X share); max over ranks"},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
