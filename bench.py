@@ -374,22 +374,19 @@ def ours_arm(args, rank: int, world: int):
     emit(line)
 
 
-_JSON_FD: int | None = None
-
-
 def claim_stdout() -> None:
     """Keep fd 1 for the one JSON line; anything native libraries write to fd 1
-    (e.g. the NCCL version banner) goes to stderr instead."""
-    global _JSON_FD
-    if _JSON_FD is None:
+    (e.g. the NCCL version banner) goes to stderr instead.  The saved fd is kept
+    in the environment because dist.py re-imports this file as `bench`."""
+    if "QRB_JSON_FD" not in os.environ:
         sys.stdout.flush()
-        _JSON_FD = os.dup(1)
+        os.environ["QRB_JSON_FD"] = str(os.dup(1))
         os.dup2(2, 1)
 
 
 def emit(line: dict) -> None:
     sys.stdout.flush()
-    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+    os.write(int(os.environ.get("QRB_JSON_FD", "1")), (json.dumps(line) + "\n").encode())
 
 
 def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
