@@ -53,56 +53,22 @@ struct SdBuf {
   int bad;
 };
 
-// x[q] -= m[g + 4q] * f for the chunks that contain a row > lo
-__device__ __forceinline__ void sweep_update(double (&x)[32], const double* m, int g, int lo,
-                                             double f) {
-#pragma unroll
-  for (int qc = 0; qc < 32; qc += 8) {
-    if (g + 4 * (qc + 7) > lo) {
-      double mv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[qc + u] = __fma_rn(-mv[u], f, x[qc + u]);
-    }
-  }
+// reciprocal: hardware approximation + two Newton steps (off the IEEE
+// division's slow path; within an ulp, which the tolerances allow)
+__device__ __forceinline__ double frcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = __fma_rn(-d, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-d, r, 1.0);
+  return __fma_rn(r, e, r);
 }
 
-// same, for the chunks that contain a row < hi
-__device__ __forceinline__ void sweep_update_below(double (&x)[32], const double* m, int g, int hi,
-                                                   double f) {
-#pragma unroll
-  for (int qc = 0; qc < 32; qc += 8) {
-    if (g + 4 * qc < hi) {
-      double mv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) mv[u] = m[g + 4 * (qc + u)];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[qc + u] = __fma_rn(-mv[u], f, x[qc + u]);
-    }
-  }
-}
-
-// value of row r (r % 4 == g) of this thread's column
-__device__ __forceinline__ double row_of(const double (&x)[32], int r) {
-  const int qr = r >> 2;
-  double v = 0.0;
-#pragma unroll
-  for (int q = 0; q < 32; ++q)
-    if (q == qr) v = x[q];
-  return v;
-}
-__device__ __forceinline__ void set_row(double (&x)[32], int r, double v) {
-  const int qr = r >> 2;
-#pragma unroll
-  for (int q = 0; q < 32; ++q)
-    if (q == qr) x[q] = v;
-}
-
-// X = U^-1 (x[q] = X(g + 4q, c)) for U upper with unit-free diagonal in
-// sb.rec (reciprocals) and strictly upper part in shared memory u (ld lu,
-// diagonal and lower part stored as zero).  Bottom-up Gauss-Jordan: the
-// unscaled row k of X eliminates U(i, k) for i < k; its owners then scale it.
+// X = U^-1 (x[q] = X(g + 4q, c)) for U upper: strictly upper part in shared
+// memory u (ld lu, diagonal and lower part stored as zero), reciprocals of the
+// diagonal in sb.rec.  Bottom-up Gauss-Jordan: the unscaled row k of X
+// eliminates U(i, k) for i < k; its owners then scale it.  Row k-1 (needed by
+// the next step) is published by its owners as soon as their chunk is done.
 __device__ void inv_upper_sweep(double (&x)[32], const double* u, int lu, SdBuf& sb) {
   const int t = threadIdx.x, c = t & 127, g = t >> 7;
 #pragma unroll
@@ -112,21 +78,38 @@ __device__ void inv_upper_sweep(double (&x)[32], const double* u, int lu, SdBuf&
   for (int k = NP - 1; k >= 0; --k) {
     const double rk = sb.rec[k];
     const double f = sb.row[k & 1][c] * rk;  // X(k, c) = 0 for c < k
-    // row k-1 for the next step first (same fma as the chunk update below)
-    if (k >= 1 && g == ((k - 1) & 3))
-      sb.row[(k - 1) & 1][c] = __fma_rn(-u[(k - 1) + (size_t)k * lu], f, row_of(x, k - 1));
-    sweep_update_below(x, u + (size_t)k * lu, g, k, f);  // U(i, k), zero for i >= k
-    if (g == (k & 3)) set_row(x, k, row_of(x, k) * rk);
+    double* rown = sb.row[(k - 1) & 1];
+    const double* uk = u + (size_t)k * lu;   // U(i, k), zero for i >= k
+    const bool own_k = g == (k & 3), own_k1 = k >= 1 && g == ((k - 1) & 3);
+#pragma unroll
+    for (int qc = 0; qc < 32; qc += 8) {
+      if (g + 4 * qc <= k) {
+        double mv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) mv[v] = uk[g + 4 * (qc + v)];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) x[qc + v] = __fma_rn(-mv[v], f, x[qc + v]);
+        if (own_k && (k >> 2) >= qc && (k >> 2) < qc + 8) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            if (qc + v == (k >> 2)) x[qc + v] *= rk;
+        }
+        if (own_k1 && ((k - 1) >> 2) >= qc && ((k - 1) >> 2) < qc + 8) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            if (qc + v == ((k - 1) >> 2)) rown[c] = x[qc + v];
+        }
+      }
+    }
     __syncthreads();
   }
 }
 
 // R = chol(G) (upper, G = R^T R) and R^-1, both written b x b with zero lower part.
-// One sweep of symmetric Gaussian elimination on the full G; the row operations
-// applied to B = I give B = L^-1 of G = L D L^T, so R = D^-1/2 S and
-// R^-T = D^-1/2 L^-1.  Column c keeps S(i, c) for i <= c; below the diagonal
-// it holds the symmetric Schur complement until step c, when it turns into
-// B(i, c) = -S(i, c) / d_c, and is then updated as B with the same formula.
+// One sweep of symmetric elimination on the upper triangle S of G; the same
+// row operations applied to B = I (strictly lower part of the same columns)
+// give B = L^-1 of G = L D L^T, so R = D^-1/2 S and R^-T = D^-1/2 L^-1.
+// Column c > k updates rows k < i <= c (S), column c <= k rows i > k (B).
 __global__ void __launch_bounds__(SD_THREADS, 1)
     chol_inv_kernel(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, int* flag,
                     int bit, int check_identity) {
@@ -139,12 +122,12 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   for (int q = 0; q < 32; ++q) {
     const int i = g + 4 * q;
     double v = (i == c) ? 1.0 : 0.0;
-    if (i < b && c < b) {
-      v = G[min(i, c) + (int64_t)max(i, c) * ldg];  // upper triangle, mirrored
+    if (i <= c && c < b) {
+      v = G[i + (int64_t)c * ldg];
       const double e = v - (i == c ? 1.0 : 0.0);
-      fro += e * e;
+      fro += (i == c ? 1.0 : 2.0) * e * e;
     }
-    x[q] = v;
+    x[q] = v;  // upper: G (identity padding); strictly lower: B = 0
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
@@ -164,36 +147,47 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
       d = 1.0;
     }
     sb.piv[0] = d;
-    sb.rec[0] = 1.0 / d;
+    sb.rec[0] = frcp(d);
   }
   __syncthreads();
   for (int k = 0; k < NP; ++k) {
     const double rk = sb.rec[k];
-    const double* mul = sb.mul[k & 1];
-    const double f = sb.row[k & 1][c] * rk;
-    // row k+1 and pivot k+1 for the next step first (same arithmetic as below)
-    if (k + 1 < NP && g == ((k + 1) & 3)) {
-      double v = row_of(x, k + 1);
-      v = c != k ? __fma_rn(-mul[k + 1], f, v) : v * -rk;
-      sb.row[(k + 1) & 1][c] = v;
-      sb.mul[(k + 1) & 1][c] = c > k + 1 ? v : 0.0;
-      if (c == k + 1) {
-        double d = v;
-        if (!(d > 0.0 && d < INFINITY)) {
-          sb.bad = 1;
-          d = 1.0;
-        }
-        sb.piv[c] = d;
-        sb.rec[c] = 1.0 / d;
-      }
-    }
-    if (c != k) {
-      sweep_update(x, mul, g, k, f);
-    } else {
-      // column k: below the diagonal S(i, k) -> B(i, k) = -S(i, k) / d_k
+    const double* mul = sb.mul[k & 1];       // S(k, i) for i > k, else 0
+    double* rown = sb.row[(k + 1) & 1];
+    double* muln = sb.mul[(k + 1) & 1];
+    const double f = (c == k ? 1.0 : sb.row[k & 1][c]) * rk;
+    const int lim = c > k ? c : NP;          // S rows stop at the diagonal
+    const int k1 = k + 1, q1 = k1 >> 2;
+    const bool pub = k1 < NP && g == (k1 & 3);
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (g + 4 * q > k) x[q] *= -rk;
+    for (int qc = 0; qc < 32; qc += 8) {
+      if (g + 4 * (qc + 7) > k) {
+        double mv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) mv[v] = mul[g + 4 * (qc + v)];
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          if (g + 4 * (qc + v) <= lim) x[qc + v] = __fma_rn(-mv[v], f, x[qc + v]);
+        if (pub && q1 >= qc && q1 < qc + 8) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            if (qc + v == q1) {
+              const double y = x[qc + v];
+              rown[c] = y;
+              muln[c] = c > k1 ? y : 0.0;
+              if (c == k1) {
+                double d = y;
+                if (!(d > 0.0 && d < INFINITY)) {
+                  sb.bad = 1;
+                  d = 1.0;
+                }
+                sb.piv[c] = d;
+                sb.rec[c] = frcp(d);
+              }
+            }
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -254,26 +248,56 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   }
   __syncthreads();
   for (int k = 0; k < NP; ++k) {
-    const double rk = sb.rec[k];
-    const double* mul = sb.mul[k & 1];
+    const double rk = sb.rec[k], pk = sb.piv[k];
+    const double* mul = sb.mul[k & 1];       // A(i, k) for i > k, else 0
+    double* rown = sb.row[(k + 1) & 1];
+    double* muln = sb.mul[(k + 1) & 1];
     const double f = c > k ? sb.row[k & 1][c] * rk : 0.0;
-    // row k+1 and pivot k+1 for the next step first (same arithmetic as below)
-    if (k + 1 < NP && g == ((k + 1) & 3) && c > k) {
-      const double v = __fma_rn(-mul[k + 1], f, row_of(x, k + 1));
-      sb.row[(k + 1) & 1][c] = v;
-      if (c == k + 1) pivot(k + 1, v);
-    }
-    if (c > k) {
-      sweep_update(x, mul, g, k, f);  // A(i,c) -= A(i,k)/p_k A(k,c)
-      if (c == k + 1) {
+    const int k1 = k + 1, q1 = k1 >> 2;
+    const bool pub_row = k1 < NP && g == (k1 & 3) && c > k;
+    const bool pub_col = c == k1;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) sb.mul[(k + 1) & 1][g + 4 * q] = (g + 4 * q > k + 1) ? x[q] : 0.0;
+    for (int qc = 0; qc < 32; qc += 8) {
+      if (g + 4 * (qc + 7) >= k) {
+        double mv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) mv[v] = mul[g + 4 * (qc + v)];
+        if (c > k) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) x[qc + v] = __fma_rn(-mv[v], f, x[qc + v]);
+        } else if (c == k) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const int i = g + 4 * (qc + v);
+            if (i > k) x[qc + v] *= rk;      // column k becomes L(:, k)
+            if (i == k) x[qc + v] = pk;      // U(k, k)
+          }
+        }
+        if (pub_col) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const int i = g + 4 * (qc + v);
+            muln[i] = i > k1 ? x[qc + v] : 0.0;
+          }
+        }
+        if (pub_row && q1 >= qc && q1 < qc + 8) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            if (qc + v == q1) {
+              rown[c] = x[qc + v];
+              if (c == k1) {
+                const double w = x[qc + v];
+                const double sgn = w >= 0.0 ? 1.0 : -1.0;
+                const double p = w + sgn;
+                sb.sg[k1] = -sgn;
+                sb.piv[k1] = p;
+                sb.rec[k1] = frcp(p);
+                if (!(fabs(w) < INFINITY)) sb.bad = 1;
+              }
+            }
+          }
+        }
       }
-    } else if (c == k) {
-#pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (g + 4 * q > k) x[q] *= rk;  // column k becomes L(:, k)
-      if (g == (k & 3)) set_row(x, k, sb.piv[k]);
     }
     __syncthreads();
   }

@@ -216,7 +216,7 @@ static int g_panel_algo = [] {
   const char* e = std::getenv("QRB_PANEL_ALGO");
   return e ? std::atoi(e) : 0;
 }();
-static int64_t g_cholqr_min_rows = 32768;  // measured crossover vs the Householder panel (r01)
+static int64_t g_cholqr_min_rows = 1024;  // CholeskyQR2 wins from ~2k rows up (r01 sweep)
 static std::atomic<int64_t> g_cholqr_panels{0}, g_cholqr_fallbacks{0};
 
 // CholeskyQR2 + Householder reconstruction of an m x b panel (cholqr.cu header
