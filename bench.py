@@ -115,6 +115,15 @@ class ClockSampler:
 # -- workload ------------------------------------------------------------------------------
 
 
+def workload_config(cfg: int, m: int, n: int, slices: int, nb: int) -> dict:
+    """The `config` object both arms report (same workload, same keys)."""
+    return {"workload": f"config{cfg}: QR of A {m}x{n} fp64 + solve {slices} slices",
+            "m": m, "n": n, "slices": slices, "panel_width": nb,
+            "parallelism": "single GPU",
+            "l2": ("inputs (A = %.1f GB) larger than L2 (126 MB)" % (m * n * 8 / 1e9))
+                  if m * n * 8 > 126e6 else "inputs fit in L2 (small configuration)"}
+
+
 def build_workload(cfg: int, slices: int | None, host_coo: bool = True):
     from paper_1907_01891_b200 import ct_system as cs
     g = cs.config_geometry(cfg)
@@ -159,6 +168,8 @@ def reference_arm(args, rank: int):
     if rank != 0:
         return
     g, coo, _, _ = build_workload(args.config, 1)
+    from paper_1907_01891_b200 import ct_system as cs
+    S = args.slices or cs.CONFIGS[args.config]["slices"]
     cores = len(os.sched_getaffinity(0))
     for _ in range(args.warmup):
         cpu_sample_tflops(coo, g)
@@ -168,9 +179,10 @@ def reference_arm(args, rank: int):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Siddon fan-beam A, seeded)",
-        "config": {"workload": f"config{args.config}: QR sample = leading {g.n_rays}x{ncol} "
-                               f"column block of A", "m": g.n_rays, "n": ncol,
-                   "tile_size": 1024, "inner_block": 128},
+        "config": {**workload_config(args.config, g.n_rays, g.n_pixels, S, args.nb),
+                   "sample": f"each step: the reference algorithm (oracle port, tile 1024, "
+                             f"inner block 128) on the leading {g.n_rays}x{ncol} column block "
+                             f"of A; TFLOP/s = 2*m*n^2 - 2n^3/3 of that block / its time"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
                                    f"({g.n_rays}x{ncol}), b=1024, w=128"},
@@ -354,10 +366,7 @@ def ours_arm(args, rank: int, world: int):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Siddon fan-beam A from seeded geometry; seeded 10-ellipse phantoms, "
                 "1% Gaussian noise)",
-        "config": {"workload": f"config{args.config}: QR of A {m}x{n} fp64 + solve {S} slices",
-                   "m": m, "n": n, "slices": S, "panel_width": args.nb,
-                   "parallelism": "single GPU",
-                   "l2": "inputs (A = %.1f GB) larger than L2 (126 MB)" % (m * n * 8 / 1e9)},
+        "config": workload_config(args.config, m, n, S, args.nb),
         "pct_fp64_peak": value / FP64_PEAK_TFLOPS,
         "slices_per_s": slices_per_s,
         "solve_tflops": solve_flops(m, n, S) / (s_ms * 1e-3) / 1e12,
