@@ -306,6 +306,7 @@ struct NnArgs {
   int mask_a;
   int group_m;
   int num_tiles;
+  int* counter;  // dynamic tile scheduler (async-epilogue kernel); nullptr = static
 };
 
 __device__ __forceinline__ void decode_tile(int tile, int num_m, int num_n, int group_m,
@@ -601,6 +602,10 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   uint64_t* empty = full + AE_STAGES;
   uint64_t* sfull = empty + AE_STAGES;
   uint64_t* sempty = sfull + 2;
+  // tile id travelling with every ring stage (producer -> consumers) and with
+  // every staged result (consumers -> epilogue warp); -1 = no more tiles
+  volatile int* stage_tile = reinterpret_cast<volatile int*>(sempty + 2);
+  volatile int* sbuf_tile = stage_tile + AE_STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -625,13 +630,30 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
     if (lane == 0) {
       prefetch_tmap(&mapA);
       prefetch_tmap(&mapB);
+      // Tiles: the first one static, then one ticket per tile from a global
+      // counter (fetched a tile ahead).  CTAs that start late -- e.g. behind a
+      // NCCL kernel holding a few SMs -- simply take fewer tiles.
+      auto next_tile = [&](int cur) {
+        if (cur >= args.num_tiles) return args.num_tiles;
+        return args.counter ? (int)gridDim.x + atomicAdd(args.counter, 1) : cur + (int)gridDim.x;
+      };
       int kit = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+      int tile = blockIdx.x;
+      int nxt = next_tile(tile);
+      for (;;) {
+        if (tile >= args.num_tiles) {  // sentinel stage: consumers stop
+          const int s = kit % AE_STAGES;
+          if (kit >= AE_STAGES) mbar_wait(&empty[s], ((kit / AE_STAGES) & 1) ^ 1);
+          stage_tile[s] = -1;
+          mbar_arrive(&full[s]);
+          break;
+        }
         int m_tile, n_tile;
         decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
         for (int kt = 0; kt < num_k; ++kt, ++kit) {
           const int s = kit % AE_STAGES;
           if (kit >= AE_STAGES) mbar_wait(&empty[s], ((kit / AE_STAGES) & 1) ^ 1);
+          stage_tile[s] = tile;
           uint8_t* sA = smem + s * NN_STAGE_BYTES;
           uint8_t* sB = sA + NN_A_BYTES;
           mbar_arrive_expect_tx(&full[s], NN_STAGE_BYTES);
@@ -641,18 +663,21 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
             tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
           tma_load_2d(sB, &mapB, k, n_tile * NN_BN, &full[s]);
         }
+        tile = nxt;
+        nxt = next_tile(tile);
       }
     }
     return;
   }
   if (warp == CONSUMER_WARPS + 1) {  // ---- epilogue warp: bulk L2 reductions ----
-    int it = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int sb = it % AE_SBUF;
+      mbar_wait(&sfull[sb], (it / AE_SBUF) & 1);
+      const int tile = sbuf_tile[sb];
+      if (tile < 0) break;
       int m_tile, n_tile;
       decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
-      const int sb = it % AE_SBUF;
       const int mg0 = m_tile * BM, ng0 = n_tile * NN_BN;
-      mbar_wait(&sfull[sb], (it / AE_SBUF) & 1);
       const uint8_t* stage = stage0 + sb * RA_STAGING;
       const int rows = min(BM, args.M - mg0);
 #pragma unroll
@@ -681,8 +706,23 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (NN_BN / 2);
-  int kit = 0, it = 0;
-  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+  int kit = 0;
+  for (int it = 0;; ++it) {
+    // the tile id arrives with the first ring stage of the tile
+    {
+      const int s0 = kit % AE_STAGES;
+      mbar_wait(&full[s0], (kit / AE_STAGES) & 1);
+    }
+    const int tile = stage_tile[kit % AE_STAGES];
+    if (tile < 0) {
+      // pass the end marker on to the epilogue warp (after its last staging)
+      const int sb = it % AE_SBUF;
+      if (it >= AE_SBUF) mbar_wait(&sempty[sb], ((it / AE_SBUF) - 1) & 1);
+      if (lane == 0 && warp == 0) sbuf_tile[sb] = -1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[sb]);
+      break;
+    }
     int m_tile, n_tile;
     decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
     const int mg0 = m_tile * BM;
@@ -721,6 +761,7 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
         }
       }
     }
+    if (lane == 0 && warp == 0) sbuf_tile[sb] = tile;
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&sfull[sb]);
@@ -885,7 +926,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     CUtensorMap ma, mb;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
-    NnArgs args;
+    NnArgs args{};
     args.M = M;
     args.N = N;
     args.K = K;
@@ -895,6 +936,18 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     const int num_n = (N + NN_BN - 1) / NN_BN;
     args.num_tiles = num_m * num_n;
     const int grid = std::min(args.num_tiles, gemm_sm_count());
+    // tile tickets: one zeroed counter per launch from a ring (launches on
+    // different streams never share one while in flight)
+    static const bool static_sched = std::getenv("QRB_NN_STATIC") != nullptr;
+    args.counter = nullptr;
+    if (!static_sched && args.num_tiles > grid) {
+      constexpr int RING = 4096;
+      static int* ring = nullptr;
+      static int slot = 0;
+      if (!ring) QRB_CUDA_TRY(cudaMalloc(&ring, RING * 32 * sizeof(int)));
+      args.counter = ring + 32 * (slot++ % RING);  // one 128-byte line each
+      QRB_CUDA_TRY(cudaMemsetAsync(args.counter, 0, sizeof(int), stream));
+    }
     gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
     QRB_CUDA_TRY(cudaGetLastError());
     return QRB_OK;
@@ -910,7 +963,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     CUtensorMap ma, mb;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
-    NnArgs args;
+    NnArgs args{};
     args.M = M;
     args.N = N;
     args.K = K;
@@ -935,7 +988,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
     QRB_TRY(make_map(&mc, MatView{out, M, N, ldo}, 16, NN_BN));
-    NnArgs args;
+    NnArgs args{};
     args.M = M;
     args.N = N;
     args.K = K;
