@@ -26,6 +26,8 @@
 #include "common.cuh"
 #include "gemm.h"
 
+#include <atomic>
+
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -943,9 +945,9 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     if (!static_sched && args.num_tiles > grid) {
       constexpr int RING = 4096;
       static int* ring = nullptr;
-      static int slot = 0;
+      static std::atomic<unsigned> slot{0};
       if (!ring) QRB_CUDA_TRY(cudaMalloc(&ring, RING * 32 * sizeof(int)));
-      args.counter = ring + 32 * (slot++ % RING);  // one 128-byte line each
+      args.counter = ring + 32 * (slot.fetch_add(1) % RING);  // one 128-byte line each
       QRB_CUDA_TRY(cudaMemsetAsync(args.counter, 0, sizeof(int), stream));
     }
     gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
