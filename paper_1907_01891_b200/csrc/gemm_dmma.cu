@@ -944,9 +944,17 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     args.counter = nullptr;
     if (!static_sched && args.num_tiles > grid) {
       constexpr int RING = 4096;
-      static int* ring = nullptr;
+      static int* rings[64] = {nullptr};  // per device
+      static std::mutex ring_mu;
       static std::atomic<unsigned> slot{0};
-      if (!ring) QRB_CUDA_TRY(cudaMalloc(&ring, RING * 32 * sizeof(int)));
+      int dev = 0;
+      QRB_CUDA_TRY(cudaGetDevice(&dev));
+      int* ring;
+      {
+        std::lock_guard<std::mutex> lk(ring_mu);
+        if (!rings[dev & 63]) QRB_CUDA_TRY(cudaMalloc(&rings[dev & 63], RING * 32 * sizeof(int)));
+        ring = rings[dev & 63];
+      }
       args.counter = ring + 32 * (slot.fetch_add(1) % RING);  // one 128-byte line each
       QRB_CUDA_TRY(cudaMemsetAsync(args.counter, 0, sizeof(int), stream));
     }
