@@ -374,10 +374,6 @@ int chol_inv(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, 
     set_last_error("chol_inv: b must be in [1, 128]");
     return QRB_ERR_ARG;
   }
-  static bool configured = false;
-  if (!configured) {
-    configured = true;
-  }
   chol_inv_kernel<<<1, SD_THREADS, 0, stream>>>(G, ldg, b, R, Rinv, ldo, flag, bit,
                                                           check_identity);
   QRB_CUDA_TRY(cudaGetLastError());
@@ -391,12 +387,7 @@ int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, doub
     set_last_error("modified_lu: b must be in [1, 128]");
     return QRB_ERR_ARG;
   }
-  static bool configured = false;
-  if (!configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sd_smem(128)));
-    configured = true;
-  }
+  QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(tri_inv_kernel), sd_smem(128)));
   mlu_kernel<<<1, SD_THREADS, 0, stream>>>(Qt, ldq, b, Uc, NUcS, L1, s, ldo, flag, bit);
   QRB_CUDA_TRY(cudaGetLastError());
   tri_inv_kernel<<<2, SD_THREADS, sd_smem(b), stream>>>(Uc, L1, b, Ucinv, L1invT, ldo, flag, bit);

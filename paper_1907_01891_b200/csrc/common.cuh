@@ -45,6 +45,11 @@ void set_last_error(const std::string& msg);
     if (_s != 0) return _s;    \
   } while (0)
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: raise
+// it once per (kernel, device), growing only.
+int set_max_dynamic_smem(const void* func, size_t bytes);
+
+
 // ---------------------------------------------------------------------------
 // column-major matrix view (device memory); ld in elements
 // ---------------------------------------------------------------------------

@@ -824,12 +824,8 @@ int launch(const MatView& a, const MatView& b, double* out, int64_t ldo, int64_t
            int M, int N, int K, int splits, int mask_a, int mask_b, cudaStream_t stream,
            int* used = nullptr) {
   constexpr int SMEM = STAGES * (BM * BK * 8 + BN * BK * 8) + 2 * STAGES * 8 + 1024;
-  static bool configured = false;
-  if (!configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_dmma_kernel<A_KMAJOR, BN, EPI>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    configured = true;
-  }
+  QRB_TRY(set_max_dynamic_smem(
+      reinterpret_cast<const void*>(gemm_dmma_kernel<A_KMAJOR, BN, EPI>), SMEM));
   CUtensorMap ma, mb;
   if (A_KMAJOR)
     QRB_TRY(make_map(&ma, a, BK, BM));
@@ -919,12 +915,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   static const bool asyncepi = std::getenv("QRB_NN_SYNC_EPI") == nullptr;
   if (epi == GEMM_EPI_SUB && asyncepi && !(std::getenv("QRB_NN_STAGED_C")) &&
       !(std::getenv("QRB_NN_CLASSIC"))) {
-    static bool configured_ae = false;
-    if (!configured_ae) {
-      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_asyncepi,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, AE_SMEM));
-      configured_ae = true;
-    }
+    QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(gemm_nn_sub_asyncepi), AE_SMEM));
     CUtensorMap ma, mb;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
@@ -964,12 +955,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   }
   static const bool redadd = std::getenv("QRB_NN_STAGED_C") == nullptr;
   if (epi == GEMM_EPI_SUB && redadd && !(std::getenv("QRB_NN_CLASSIC"))) {
-    static bool configured_ra = false;
-    if (!configured_ra) {
-      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_redadd,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, RA_SMEM));
-      configured_ra = true;
-    }
+    QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(gemm_nn_sub_redadd), RA_SMEM));
     CUtensorMap ma, mb;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
@@ -988,12 +974,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     return QRB_OK;
   }
   if (epi == GEMM_EPI_SUB && !(std::getenv("QRB_NN_CLASSIC"))) {
-    static bool configured = false;
-    if (!configured) {
-      QRB_CUDA_TRY(cudaFuncSetAttribute(gemm_nn_sub_persistent,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, NN_SMEM));
-      configured = true;
-    }
+    QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(gemm_nn_sub_persistent), NN_SMEM));
     CUtensorMap ma, mb, mc;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));

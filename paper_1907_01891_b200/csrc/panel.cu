@@ -499,13 +499,7 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
     fn = reinterpret_cast<void*>(panel_qr_kernel<4>);
   else
     fn = reinterpret_cast<void*>(panel_qr_kernel<8>);
-  static size_t configured[4] = {0, 0, 0, 0};
-  const int slot = own <= 1 ? 0 : own <= 2 ? 1 : own <= 4 ? 2 : 3;
-  if (smem > configured[slot]) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-    configured[slot] = smem;
-  }
+  QRB_TRY(set_max_dynamic_smem(fn, smem));
   QRB_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned int), stream));
   PanelArgs a;
   a.A = panel.ptr;
@@ -554,12 +548,7 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
 int build_t(const double* G, int ldg, const double* tau, int w, double* T, int ldt,
             cudaStream_t stream) {
   const size_t smem = ((size_t)w * w + (size_t)w * 32) * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-    configured = smem;
-  }
+  QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(build_t_kernel), smem));
   build_t_kernel<<<1, BT_THREADS, smem, stream>>>(G, ldg, tau, w, T, ldt);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
@@ -579,13 +568,7 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
 int trtri_blocks(const double* A, int64_t lda, int n, int bs, double* Rinv, cudaStream_t stream) {
   const int nblk = (n + bs - 1) / bs;
   const size_t smem = (size_t)bs * bs * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    QRB_CUDA_TRY(cudaFuncSetAttribute(trtri_blocks_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-    configured = smem;
-  }
+  QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(trtri_blocks_kernel), smem));
   trtri_blocks_kernel<<<nblk, 128, smem, stream>>>(A, lda, n, bs, Rinv);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
