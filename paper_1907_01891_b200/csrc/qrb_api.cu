@@ -738,7 +738,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
   cudaStream_t st = h->stream;
   const int nb = h->nb;
   int64_t W = chunk_cols;
-  if (W == 0) W = std::max<int64_t>(8192, (h->n / 8 + nb - 1) / nb * nb);
+  if (W == 0) W = 4096;  // measured best at config 3 (2048..32768 swept)
   W = std::max<int64_t>(nb, (W + nb - 1) / nb * nb);
   const int64_t nchunks = (h->n + W - 1) / W;
   cudaStream_t cs = nullptr;
@@ -783,8 +783,33 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     QRB_TRY(ws.bar.ensure(64, st));
     int* nf = static_cast<int*>(ws.bar.p) + 8;
     QRB_CUDA_TRY(cudaMemsetAsync(nf, 0, sizeof(int), st));
+    static const bool no_switch = std::getenv("QRB_E2E_NO_SWITCH") != nullptr;
     for (int64_t c = 0; c < nchunks && status == QRB_OK; ++c) {
       const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
+      if (c > 0 && !no_switch && cudaEventQuery(landed[nchunks - 1]) == cudaSuccess) {
+        // the whole matrix has landed: finish in the right-looking order (the
+        // remaining columns catch up on every earlier panel with wide GEMMs,
+        // then the usual panel + trailing-update steps)
+        const int64_t rem = h->n - col0;
+        QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[nchunks - 1], 0));
+        nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, rem, nf);
+        g_launches += 1;
+        const int kc0 = static_cast<int>(col0 / nb);
+        for (int k = 0; k < kc0 && status == QRB_OK; ++k) {
+          const int64_t j0 = int64_t(k) * nb, mk = h->m - j0;
+          status = apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
+                            A.sub(j0, col0, mk, rem), ws, st);
+        }
+        for (int64_t j0 = col0; j0 < h->n && status == QRB_OK; j0 += nb) {
+          const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
+          double* Tk = h->T + (j0 / nb) * nb * nb;
+          status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
+          if (status == QRB_OK && j0 + pw < h->n)
+            status = apply_qt(A.sub(j0, j0, mk, pw), Tk, nb,
+                              A.sub(j0, j0 + pw, mk, h->n - j0 - pw), ws, st);
+        }
+        break;
+      }
       QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[c], 0));
       nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, nc, nf);
       g_launches += 1;
