@@ -21,6 +21,11 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
             int epi, int mask_a, cudaStream_t stream);
 
 int gemm_pick_splits(int M, int N, int K, int max_splits);
+
+// dynamic tile tickets for the persistent NN update (multi-GPU runs, where an
+// NCCL kernel can hold SMs while the update starts); static otherwise
+void gemm_set_nn_dynamic(bool on);
+bool gemm_nn_dynamic();
 int gemm_sm_count();
 
 }  // namespace qrb

@@ -604,6 +604,150 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   uint64_t* empty = full + AE_STAGES;
   uint64_t* sfull = empty + AE_STAGES;
   uint64_t* sempty = sfull + 2;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + NN_BN - 1) / NN_BN;
+  const int num_k = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < AE_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sfull[b], CONSUMER_WARPS);
+      mbar_init(&sempty[b], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CONSUMER_WARPS) {  // ---- TMA producer ----
+    if (lane == 0) {
+      prefetch_tmap(&mapA);
+      prefetch_tmap(&mapB);
+      int kit = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        int m_tile, n_tile;
+        decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+        for (int kt = 0; kt < num_k; ++kt, ++kit) {
+          const int s = kit % AE_STAGES;
+          if (kit >= AE_STAGES) mbar_wait(&empty[s], ((kit / AE_STAGES) & 1) ^ 1);
+          uint8_t* sA = smem + s * NN_STAGE_BYTES;
+          uint8_t* sB = sA + NN_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], NN_STAGE_BYTES);
+          const int k = kt * BK;
+#pragma unroll
+          for (int mb = 0; mb < BM / 16; ++mb)
+            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+          tma_load_2d(sB, &mapB, k, n_tile * NN_BN, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == CONSUMER_WARPS + 1) {  // ---- epilogue warp: bulk L2 reductions ----
+    int it = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      int m_tile, n_tile;
+      decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+      const int sb = it % AE_SBUF;
+      const int mg0 = m_tile * BM, ng0 = n_tile * NN_BN;
+      mbar_wait(&sfull[sb], (it / AE_SBUF) & 1);
+      const uint8_t* stage = stage0 + sb * RA_STAGING;
+      const int rows = min(BM, args.M - mg0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = lane + 32 * h;
+        if (ng0 + n < args.N && rows > 0) {
+          double* dst = C + mg0 + static_cast<int64_t>(ng0 + n) * ldc;
+          const int even = rows & ~1;
+          if (even) bulk_reduce_add_f64(dst, stage + n * RA_COL_BYTES, even * 8);
+          if (rows & 1)
+            atomicAdd(dst + even,
+                      *reinterpret_cast<const double*>(stage + n * RA_COL_BYTES + even * 8));
+        }
+      }
+      bulk_commit();
+      bulk_wait_read0();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sb]);
+    }
+    bulk_wait0();
+    return;
+  }
+
+  // ---- consumer warps: DMMA main loop, stage -acc, arrive ----
+  const int g = lane >> 2;
+  const int q = lane & 3;
+  const int m0 = (warp & 3) * 32;
+  const int n0 = (warp >> 2) * (NN_BN / 2);
+  int kit = 0, it = 0;
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    int m_tile, n_tile;
+    decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
+    const int mg0 = m_tile * BM;
+    const int ng0 = n_tile * NN_BN;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < num_k; ++kt, ++kit) {
+      const int s = kit % AE_STAGES;
+      mbar_wait(&full[s], (kit / AE_STAGES) & 1);
+      const uint8_t* sA = smem + s * NN_STAGE_BYTES;
+      const uint8_t* sB = sA + NN_A_BYTES;
+      const int kg0 = kt * BK;
+      if (args.mask_a && mg0 <= kg0 + BK - 1)
+        consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      else
+        consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const int sb = it % AE_SBUF;
+    if (it >= AE_SBUF) mbar_wait(&sempty[sb], ((it / AE_SBUF) - 1) & 1);
+    uint8_t* stage = stage0 + sb * RA_STAGING;
+#pragma unroll
+    for (int mp = 0; mp < 2; ++mp) {
+      const int m = m0 + mp * 16 + 2 * g;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + nt * 8 + rp(2 * q + e);
+          *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
+              make_double2(-acc[mp * 2 + 0][nt][e], -acc[mp * 2 + 1][nt][e]);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sfull[sb]);
+  }
+}
+
+// Same kernel with dynamic tile tickets (first tile static, then a per-launch
+// global counter; the tile id travels through the smem ring).  CTAs that start
+// late -- e.g. behind an NCCL kernel holding a few SMs on a multi-GPU run --
+// take fewer tiles instead of stretching the launch.  Selected with
+// qrb_set_tuning("nn_dynamic", 1) (dist.py does so on more than one GPU); on
+// an idle GPU the static schedule above is ~1% faster (r01 A/B in bench.py).
+__global__ void __launch_bounds__(AE_THREADS, 1)
+    gemm_nn_sub_asyncepi_dyn(const __grid_constant__ CUtensorMap mapA,
+                         const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
+                         const int64_t ldc, const NnArgs args) {
+  constexpr int NT = NN_BN / 16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stage0 = smem + AE_STAGES * NN_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + AE_SBUF * RA_STAGING);
+  uint64_t* empty = full + AE_STAGES;
+  uint64_t* sfull = empty + AE_STAGES;
+  uint64_t* sempty = sfull + 2;
   // tile id travelling with every ring stage (producer -> consumers) and with
   // every staged result (consumers -> epilogue warp); -1 = no more tiles
   volatile int* stage_tile = reinterpret_cast<volatile int*>(sempty + 2);
@@ -905,6 +1049,10 @@ int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ld
                                           mask_a, mask_b, stream, used);
 }
 
+static std::atomic<bool> g_nn_dynamic{false};
+void gemm_set_nn_dynamic(bool on) { g_nn_dynamic.store(on); }
+bool gemm_nn_dynamic() { return g_nn_dynamic.load(); }
+
 int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int M, int N, int K,
             int epi, int mask_a, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
@@ -915,7 +1063,10 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   static const bool asyncepi = std::getenv("QRB_NN_SYNC_EPI") == nullptr;
   if (epi == GEMM_EPI_SUB && asyncepi && !(std::getenv("QRB_NN_STAGED_C")) &&
       !(std::getenv("QRB_NN_CLASSIC"))) {
-    QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(gemm_nn_sub_asyncepi), AE_SMEM));
+    const bool dyn = g_nn_dynamic.load();
+    QRB_TRY(set_max_dynamic_smem(dyn ? reinterpret_cast<const void*>(gemm_nn_sub_asyncepi_dyn)
+                                     : reinterpret_cast<const void*>(gemm_nn_sub_asyncepi),
+                                 AE_SMEM));
     CUtensorMap ma, mb;
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
@@ -929,11 +1080,15 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     const int num_n = (N + NN_BN - 1) / NN_BN;
     args.num_tiles = num_m * num_n;
     const int grid = std::min(args.num_tiles, gemm_sm_count());
+    if (!dyn) {
+      gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
+      QRB_CUDA_TRY(cudaGetLastError());
+      return QRB_OK;
+    }
     // tile tickets: one zeroed counter per launch from a ring (launches on
     // different streams never share one while in flight)
-    static const bool static_sched = std::getenv("QRB_NN_STATIC") != nullptr;
     args.counter = nullptr;
-    if (!static_sched && args.num_tiles > grid) {
+    if (args.num_tiles > grid) {
       constexpr int RING = 4096;
       static int* rings[64] = {nullptr};  // per device
       static std::mutex ring_mu;
@@ -949,7 +1104,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
       args.counter = ring + 32 * (slot.fetch_add(1) % RING);  // one 128-byte line each
       QRB_CUDA_TRY(cudaMemsetAsync(args.counter, 0, sizeof(int), stream));
     }
-    gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
+    gemm_nn_sub_asyncepi_dyn<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
     QRB_CUDA_TRY(cudaGetLastError());
     return QRB_OK;
   }

@@ -1149,6 +1149,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_cholqr_min_rows = value;
     return QRB_OK;
   }
+  if (k == "nn_dynamic" && (value == 0 || value == 1)) {
+    gemm_set_nn_dynamic(value == 1);
+    return QRB_OK;
+  }
   set_last_error("qrb_set_tuning: unknown key or bad value: " + k);
   return QRB_ERR_ARG;
 }
@@ -1161,6 +1165,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   }
   if (k == "panel_algo") *value = g_panel_algo;
   else if (k == "cholqr_min_rows") *value = g_cholqr_min_rows;
+  else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
   else if (k == "cholqr_fallbacks") *value = g_cholqr_fallbacks.load();
   else {

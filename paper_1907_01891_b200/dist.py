@@ -60,10 +60,13 @@ class CudaOps:
     """Local arithmetic through the C ABI (stream-ordered qrb_op_* calls on
     torch CUDA tensors holding column-major matrices as (cols, ld) tensors)."""
 
-    def __init__(self):
+    def __init__(self, world: int = 1):
         from . import _native
         self.lib = _native.load()
         self.native = _native
+        # with several ranks a receiver's NCCL kernel can hold SMs while the
+        # trailing update starts: let the persistent GEMM hand out tiles dynamically
+        _native.set_tuning("nn_dynamic", 1 if world > 1 else 0)
 
     @staticmethod
     def _p(t, off=0):
@@ -356,7 +359,7 @@ def bench_rank(args, rank: int, world: int):
     b_dev = torch.zeros((max(cnt, 1), lda), dtype=torch.float64, device="cuda")
     b_dev[:cnt, :m] = torch.from_numpy(np.ascontiguousarray(b_host[:, first:first + cnt].T)).cuda()
     x_dev = torch.zeros((max(cnt, 1), n + (n & 1)), dtype=torch.float64, device="cuda")
-    ops = CudaOps()
+    ops = CudaOps(world)
     # keep a pristine copy of the local panels only if it fits (config 4 at 8 GPUs
     # is ~71 GB per rank: re-densify with the Siddon kernel instead)
     free, total = torch.cuda.mem_get_info()

@@ -124,3 +124,27 @@ def test_trsm_upper(n, nb, nrhs):
     bt, ldb = to_dev(b)
     assert lib().qrb_op_trsm_upper(P(rt), ldr, n, nb, P(bt), ldb, nrhs, None) == 0
     assert rel_err(to_host(bt, n), sla.solve_triangular(r, b)) <= 1e-12
+
+
+def test_nn_dynamic_tile_schedule_is_bitwise_identical():
+    """The dynamic tile tickets (multi-GPU setting) change only which CTA
+    computes a tile: every C element still receives exactly one reduce-add per
+    launch, so the factors are bitwise identical to the static schedule."""
+    from paper_1907_01891_b200 import _native
+    from paper_1907_01891_b200.device import QrDevice
+
+    rng = np.random.default_rng(77)
+    m, n = 5000, 2300
+    a = rng.standard_normal((m, n))
+    out = {}
+    old = _native.get_tuning("nn_dynamic")
+    try:
+        for dyn in (0, 1):
+            _native.set_tuning("nn_dynamic", dyn)
+            with QrDevice(m, n) as q:
+                q.set_matrix(a)
+                q.factorize()
+                out[dyn] = q.get_matrix()
+    finally:
+        _native.set_tuning("nn_dynamic", old)
+    np.testing.assert_array_equal(out[0], out[1])
