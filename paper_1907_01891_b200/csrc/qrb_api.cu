@@ -262,7 +262,7 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
   QRB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), st));
   auto gram = [&](const MatView& X) -> int {
     const int64_t per = int64_t(LD) * b;
-    const int splits = gemm_pick_splits(b, b, m, 64);
+    const int splits = gemm_pick_splits(b, b, m, 256);  // one tile pair: use every SM
     if (splits > 1) {
       QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
       int used = 0;
@@ -365,7 +365,7 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
   }
   // Gram matrix of the whole panel, then T
   const int64_t per = int64_t(ldg) * pw;
-  const int splits = gemm_pick_splits(pw, pw, m, 64);
+  const int splits = gemm_pick_splits(pw, pw, m, 256);
   if (splits > 1) {
     QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
     int used = 0;
