@@ -81,12 +81,14 @@ struct DevBuf {
 struct Workspace {
   DevBuf part, bar, G, Ti, W, W2, Wparts;
   DevBuf Wq, small, flag;  // CholeskyQR2 panel: Q1 (m x b), 12 b x b blocks, status word
+  DevBuf T2;               // merged block reflector of a panel pair (2nb x 2nb) + scratch
   int* hflag = nullptr;    // pinned host copy of the status word
   void release() {
     if (hflag) cudaFreeHost(hflag);
     hflag = nullptr;
     Wq.release();
     small.release();
+    T2.release();
     flag.release();
     part.release();
     bar.release();
@@ -379,6 +381,67 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
   }
   QRB_TRY(build_t(ws.G.d(), ldg, tau, pw, T, static_cast<int>(ldt), st));
   g_launches += 1;
+  return QRB_OK;
+}
+
+// Two nb-wide panels merged into one 2nb-wide block reflector for the trailing
+// update: the GEMMs then run with K = 2nb, halving the NN kernel's per-tile
+// switches (NN 33.6 -> 34.7 TFLOP/s at K = 256, r01 tools/gemm_k.py).
+//   factor panel a; apply Q_a^T to panel b's columns; factor panel b;
+//   T = [[T_a, -T_a (V_a^T V_b) T_b], [0, T_b]]   (larft merge)
+// T_a / T_b are also stored per panel (the solve applies nb-wide panels).
+// Panels per outer step (qrb_set_tuning "outer_panels": 1 or 2).
+static int g_outer_panels = [] {
+  const char* e = std::getenv("QRB_OUTER_PANELS");
+  return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+}();
+
+static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
+                        cudaStream_t st);
+
+static int factor_panel_pair(const MatView& A, int64_t j0, int nb, double* Ta, double* Tb,
+                             double* tau, double** T2out, Workspace& ws, cudaStream_t st) {
+  const int64_t mk = A.rows - j0;
+  const int w2 = 2 * nb;
+  const MatView Va = A.sub(j0, j0, mk, nb);
+  QRB_TRY(factor_panel(Va, tau + j0, Ta, nb, ws, st));
+  QRB_TRY(apply_qt(Va, Ta, nb, A.sub(j0, j0 + nb, mk, nb), ws, st));
+  const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, nb);
+  QRB_TRY(factor_panel(Vb, tau + j0 + nb, Tb, nb, ws, st));
+  const int64_t LD2 = w2;
+  QRB_TRY(ws.T2.ensure(sizeof(double) * (LD2 * w2 + 3 * int64_t(nb) * nb), st));
+  double* T2 = ws.T2.d();
+  double* Y = T2 + LD2 * w2;
+  double* Z = Y + int64_t(nb) * nb;
+  // Y = V_a[nb:]^T V_b (V_a rows below its own block are plain; V_b unit lower)
+  {
+    const MatView Va_lo = A.sub(j0 + nb, j0, mk - nb, nb);
+    const int64_t per = int64_t(nb) * nb;
+    const int splits = gemm_pick_splits(nb, nb, static_cast<int>(mk - nb), 256);
+    if (splits > 1) {
+      QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+      int used = 0;
+      QRB_TRY(gemm_tn_split(Va_lo, Vb, ws.Wparts.d(), nb, per, nb, nb, static_cast<int>(mk - nb),
+                            splits, 0, 1, st, &used));
+      QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, nb, nb, nb, Y, nb, st));
+      g_launches += 2;
+    } else {
+      QRB_TRY(gemm_tn(Va_lo, Vb, Y, nb, 0, nb, nb, static_cast<int>(mk - nb), 1, 0, 1, st));
+      g_launches += 1;
+    }
+  }
+  // T2 = [[Ta, T12], [0, Tb]],  T12 = -(Ta Y) Tb
+  QRB_CUDA_TRY(cudaMemsetAsync(T2, 0, sizeof(double) * LD2 * w2, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2, sizeof(double) * LD2, Ta, sizeof(double) * nb,
+                                 sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2 + nb + LD2 * nb, sizeof(double) * LD2, Tb, sizeof(double) * nb,
+                                 sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
+  QRB_TRY(gemm_nn(MatView{Ta, nb, nb, nb}, MatView{Y, nb, nb, nb}, Z, nb, nb, nb, nb,
+                  GEMM_EPI_STORE, 0, st));
+  QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{Tb, nb, nb, nb}, T2 + LD2 * nb, LD2, nb, nb, nb,
+                  GEMM_EPI_SUB, 0, st));
+  g_launches += 2;
+  *T2out = T2;
   return QRB_OK;
 }
 
@@ -689,6 +752,18 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
     const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
     const int64_t mk = h->m - j0;
     double* Tk = h->T + int64_t(k) * h->nb * h->nb;
+    if (g_outer_panels == 2 && !timing && j0 + 2 * int64_t(h->nb) < h->n &&
+        mk >= 2 * int64_t(h->nb)) {
+      // a pair of full panels, then one trailing update with K = 2nb
+      double* T2 = nullptr;
+      QRB_TRY(factor_panel_pair(A, j0, h->nb, Tk, Tk + int64_t(h->nb) * h->nb, h->tau, &T2, ws,
+                                st));
+      const int64_t c0 = j0 + 2 * h->nb;
+      QRB_TRY(apply_qt(A.sub(j0, j0, mk, 2 * h->nb), T2, 2 * h->nb, A.sub(j0, c0, mk, h->n - c0),
+                       ws, st));
+      ++k;
+      continue;
+    }
     if (timing) cudaEventRecord(ep0, st);
     QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, h->nb, ws, st));
     if (timing) cudaEventRecord(ep1, st);
@@ -803,6 +878,15 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
         for (int64_t j0 = col0; j0 < h->n && status == QRB_OK; j0 += nb) {
           const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
           double* Tk = h->T + (j0 / nb) * nb * nb;
+          if (g_outer_panels == 2 && j0 + 2 * int64_t(nb) < h->n && mk >= 2 * int64_t(nb)) {
+            double* T2 = nullptr;
+            status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st);
+            if (status == QRB_OK)
+              status = apply_qt(A.sub(j0, j0, mk, 2 * nb), T2, 2 * nb,
+                                A.sub(j0, j0 + 2 * nb, mk, h->n - j0 - 2 * nb), ws, st);
+            j0 += nb;
+            continue;
+          }
           status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
           if (status == QRB_OK && j0 + pw < h->n)
             status = apply_qt(A.sub(j0, j0, mk, pw), Tk, nb,
@@ -1149,6 +1233,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_cholqr_min_rows = value;
     return QRB_OK;
   }
+  if (k == "outer_panels" && (value == 1 || value == 2)) {
+    g_outer_panels = static_cast<int>(value);
+    return QRB_OK;
+  }
   if (k == "nn_dynamic" && (value == 0 || value == 1)) {
     gemm_set_nn_dynamic(value == 1);
     return QRB_OK;
@@ -1166,6 +1254,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   if (k == "panel_algo") *value = g_panel_algo;
   else if (k == "cholqr_min_rows") *value = g_cholqr_min_rows;
   else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
+  else if (k == "outer_panels") *value = g_outer_panels;
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
   else if (k == "cholqr_fallbacks") *value = g_cholqr_fallbacks.load();
   else {

@@ -148,3 +148,32 @@ def test_nn_dynamic_tile_schedule_is_bitwise_identical():
     finally:
         _native.set_tuning("nn_dynamic", old)
     np.testing.assert_array_equal(out[0], out[1])
+
+
+def test_panel_pairs_match_single_panel_steps():
+    """Trailing updates with the merged 2nb-wide block reflector (outer_panels=2,
+    larft merge of two panels) give the same factors as nb-wide steps."""
+    from paper_1907_01891_b200 import _native
+    from paper_1907_01891_b200.device import QrDevice
+
+    rng = np.random.default_rng(12)
+    m, n = 3000, 1100
+    a = rng.standard_normal((m, n))
+    b = rng.standard_normal((m, 4))
+    res = {}
+    old = _native.get_tuning("outer_panels")
+    try:
+        for outer in (1, 2):
+            _native.set_tuning("outer_panels", outer)
+            with QrDevice(m, n) as q:
+                q.set_matrix(a)
+                q.factorize()
+                x, r, _ = q.solve(b)
+                res[outer] = (q.get_matrix(), x, r)
+    finally:
+        _native.set_tuning("outer_panels", old)
+    f1, f2 = res[1][0], res[2][0]
+    assert rel_err(np.triu(f2[:n]), np.triu(f1[:n])) <= 1e-12
+    assert rel_err(np.tril(f2, -1), np.tril(f1, -1)) <= 1e-11
+    assert rel_err(res[2][1], res[1][1]) <= 1e-10
+    np.testing.assert_allclose(res[2][2], res[1][2], rtol=1e-10)
