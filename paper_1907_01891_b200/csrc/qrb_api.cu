@@ -399,6 +399,45 @@ static int g_outer_panels = [] {
 static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
                         cudaStream_t st);
 
+// T2 (2nb x 2nb, leading dim ldt2) = [[Ta, -Ta (V_a[nb:]^T V_b) Tb], [0, Tb]] for the
+// factored panels a = A[j0:, j0:j0+nb] and b = A[j0+nb:, j0+nb:j0+2nb] (larft merge);
+// scratch: 2 nb x nb blocks
+static int merge_pair_t(const MatView& A, int64_t j0, int nb, const double* Ta, const double* Tb,
+                        double* T2, int64_t ldt2, double* scratch, Workspace& ws,
+                        cudaStream_t st) {
+  const int64_t mk = A.rows - j0;
+  double* Y = scratch;
+  double* Z = Y + int64_t(nb) * nb;
+  const MatView Va_lo = A.sub(j0 + nb, j0, mk - nb, nb);      // plain rows of V_a
+  const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, nb);    // unit lower V_b
+  const int64_t per = int64_t(nb) * nb;
+  const int splits = gemm_pick_splits(nb, nb, static_cast<int>(mk - nb), 256);
+  if (splits > 1) {
+    QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+    int used = 0;
+    QRB_TRY(gemm_tn_split(Va_lo, Vb, ws.Wparts.d(), nb, per, nb, nb, static_cast<int>(mk - nb),
+                          splits, 0, 1, st, &used));
+    QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, nb, nb, nb, Y, nb, st));
+    g_launches += 2;
+  } else {
+    QRB_TRY(gemm_tn(Va_lo, Vb, Y, nb, 0, nb, nb, static_cast<int>(mk - nb), 1, 0, 1, st));
+    g_launches += 1;
+  }
+  const int w2 = 2 * nb;
+  QRB_CUDA_TRY(cudaMemset2DAsync(T2, sizeof(double) * ldt2, 0, sizeof(double) * w2, w2, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2, sizeof(double) * ldt2, Ta, sizeof(double) * nb,
+                                 sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2 + nb + ldt2 * nb, sizeof(double) * ldt2, Tb,
+                                 sizeof(double) * nb, sizeof(double) * nb, nb,
+                                 cudaMemcpyDeviceToDevice, st));
+  QRB_TRY(gemm_nn(MatView{const_cast<double*>(Ta), nb, nb, nb}, MatView{Y, nb, nb, nb}, Z, nb, nb,
+                  nb, nb, GEMM_EPI_STORE, 0, st));
+  QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{const_cast<double*>(Tb), nb, nb, nb},
+                  T2 + ldt2 * nb, ldt2, nb, nb, nb, GEMM_EPI_SUB, 0, st));
+  g_launches += 2;
+  return QRB_OK;
+}
+
 static int factor_panel_pair(const MatView& A, int64_t j0, int nb, double* Ta, double* Tb,
                              double* tau, double** T2out, Workspace& ws, cudaStream_t st) {
   const int64_t mk = A.rows - j0;
@@ -408,40 +447,9 @@ static int factor_panel_pair(const MatView& A, int64_t j0, int nb, double* Ta, d
   QRB_TRY(apply_qt(Va, Ta, nb, A.sub(j0, j0 + nb, mk, nb), ws, st));
   const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, nb);
   QRB_TRY(factor_panel(Vb, tau + j0 + nb, Tb, nb, ws, st));
-  const int64_t LD2 = w2;
-  QRB_TRY(ws.T2.ensure(sizeof(double) * (LD2 * w2 + 3 * int64_t(nb) * nb), st));
-  double* T2 = ws.T2.d();
-  double* Y = T2 + LD2 * w2;
-  double* Z = Y + int64_t(nb) * nb;
-  // Y = V_a[nb:]^T V_b (V_a rows below its own block are plain; V_b unit lower)
-  {
-    const MatView Va_lo = A.sub(j0 + nb, j0, mk - nb, nb);
-    const int64_t per = int64_t(nb) * nb;
-    const int splits = gemm_pick_splits(nb, nb, static_cast<int>(mk - nb), 256);
-    if (splits > 1) {
-      QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
-      int used = 0;
-      QRB_TRY(gemm_tn_split(Va_lo, Vb, ws.Wparts.d(), nb, per, nb, nb, static_cast<int>(mk - nb),
-                            splits, 0, 1, st, &used));
-      QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, nb, nb, nb, Y, nb, st));
-      g_launches += 2;
-    } else {
-      QRB_TRY(gemm_tn(Va_lo, Vb, Y, nb, 0, nb, nb, static_cast<int>(mk - nb), 1, 0, 1, st));
-      g_launches += 1;
-    }
-  }
-  // T2 = [[Ta, T12], [0, Tb]],  T12 = -(Ta Y) Tb
-  QRB_CUDA_TRY(cudaMemsetAsync(T2, 0, sizeof(double) * LD2 * w2, st));
-  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2, sizeof(double) * LD2, Ta, sizeof(double) * nb,
-                                 sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
-  QRB_CUDA_TRY(cudaMemcpy2DAsync(T2 + nb + LD2 * nb, sizeof(double) * LD2, Tb, sizeof(double) * nb,
-                                 sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
-  QRB_TRY(gemm_nn(MatView{Ta, nb, nb, nb}, MatView{Y, nb, nb, nb}, Z, nb, nb, nb, nb,
-                  GEMM_EPI_STORE, 0, st));
-  QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{Tb, nb, nb, nb}, T2 + LD2 * nb, LD2, nb, nb, nb,
-                  GEMM_EPI_SUB, 0, st));
-  g_launches += 2;
-  *T2out = T2;
+  QRB_TRY(ws.T2.ensure(sizeof(double) * (int64_t(w2) * w2 + 3 * int64_t(nb) * nb), st));
+  QRB_TRY(merge_pair_t(A, j0, nb, Ta, Tb, ws.T2.d(), w2, ws.T2.d() + int64_t(w2) * w2, ws, st));
+  *T2out = ws.T2.d();
   return QRB_OK;
 }
 
@@ -513,6 +521,11 @@ struct qrb_handle {
   double* Rinv = nullptr;  // npanels blocks of nb x nb
   bool factored = false;
   bool rinv_ready = false;
+  double* T2 = nullptr;    // merged 2nb x 2nb reflectors of panel pairs (solve), lazily
+  bool t2_ready = false;
+  double* Rinv2 = nullptr; // inverses of the 2nb x 2nb diagonal blocks of R (pairs), lazily
+  bool rinv2_ready = false;
+  DevBuf Ytmp;             // copy of a 2nb-row block of the right-hand sides
   cudaStream_t stream = nullptr;      // stream all work of the handle is enqueued on
   cudaStream_t own_stream = nullptr;  // the handle's own stream
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -575,11 +588,134 @@ struct ProfSession {
   }
 };
 
+// merged 2nb-wide reflectors of panel pairs (2p, 2p+1), for the solve's Q^T B
+bool pair_ok(const qrb_handle* h, int k) {
+  const int64_t j0 = int64_t(k) * h->nb;
+  return g_outer_panels == 2 && (k & 1) == 0 && j0 + 2 * int64_t(h->nb) <= h->n &&
+         h->m - j0 >= 2 * int64_t(h->nb);
+}
+
+int ensure_t2(qrb_handle* h, Workspace& ws) {
+  if (h->t2_ready) return QRB_OK;
+  const int nb = h->nb;
+  const int64_t w2 = 2 * int64_t(nb), blk = w2 * w2;
+  const int npairs = h->npanels / 2;
+  if (npairs == 0) {
+    h->t2_ready = true;
+    return QRB_OK;
+  }
+  if (!h->T2) {
+    if (cudaMalloc(&h->T2, sizeof(double) * (npairs * blk + 2 * int64_t(nb) * nb)) != cudaSuccess) {
+      cudaGetLastError();
+      h->T2 = nullptr;
+      set_last_error("qrb_solve: T2 alloc failed");
+      return QRB_ENOMEM;
+    }
+  }
+  MatView A{h->A, h->m, h->n, h->lda};
+  double* scratch = h->T2 + npairs * blk;
+  for (int p = 0; p < npairs; ++p) {
+    if (!pair_ok(h, 2 * p)) continue;
+    const double* Ta = h->T + int64_t(2 * p) * nb * nb;
+    QRB_TRY(merge_pair_t(A, int64_t(2 * p) * nb, nb, Ta, Ta + int64_t(nb) * nb, h->T2 + p * blk,
+                         w2, scratch, ws, h->stream));
+  }
+  h->t2_ready = true;
+  return QRB_OK;
+}
+
 int ensure_rinv(qrb_handle* h) {
   if (h->rinv_ready) return QRB_OK;
   QRB_TRY(trtri_blocks(h->A, h->lda, static_cast<int>(h->n), h->nb, h->Rinv, h->stream));
   g_launches += 1;
   h->rinv_ready = true;
+  return QRB_OK;
+}
+
+// inverses of the 2nb x 2nb diagonal blocks of R for the panel pairs:
+// [[A, B], [0, C]]^-1 = [[A^-1, -A^-1 B C^-1], [0, C^-1]] from the nb-block inverses
+int ensure_rinv2(qrb_handle* h) {
+  if (h->rinv2_ready) return QRB_OK;
+  QRB_TRY(ensure_rinv(h));
+  const int nb = h->nb;
+  const int64_t w2 = 2 * int64_t(nb), blk = w2 * w2, nb2 = int64_t(nb) * nb;
+  const int npairs = h->npanels / 2;
+  if (npairs == 0) {
+    h->rinv2_ready = true;
+    return QRB_OK;
+  }
+  if (!h->Rinv2) {
+    if (cudaMalloc(&h->Rinv2, sizeof(double) * (npairs * blk + nb2)) != cudaSuccess) {
+      cudaGetLastError();
+      h->Rinv2 = nullptr;
+      set_last_error("qrb_solve: Rinv2 alloc failed");
+      return QRB_ENOMEM;
+    }
+  }
+  cudaStream_t st = h->stream;
+  double* Z = h->Rinv2 + npairs * blk;
+  for (int p = 0; p < npairs; ++p) {
+    const int k = 2 * p;
+    if (!pair_ok(h, k)) continue;
+    const int64_t j0 = int64_t(k) * nb;
+    double* D = h->Rinv2 + p * blk;
+    const double* Ai = h->Rinv + int64_t(k) * nb2;
+    const double* Ci = Ai + nb2;
+    QRB_CUDA_TRY(cudaMemset2DAsync(D, sizeof(double) * w2, 0, sizeof(double) * w2, w2, st));
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(D, sizeof(double) * w2, Ai, sizeof(double) * nb,
+                                   sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(D + nb + w2 * nb, sizeof(double) * w2, Ci, sizeof(double) * nb,
+                                   sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
+    // Z = A^-1 B, B = R[j0:j0+nb, j0+nb:j0+2nb];  D12 = -Z C^-1
+    const MatView Bblk{h->A + j0 + (j0 + nb) * h->lda, nb, nb, h->lda};
+    QRB_TRY(gemm_nn(MatView{const_cast<double*>(Ai), nb, nb, nb}, Bblk, Z, nb, nb, nb, nb,
+                    GEMM_EPI_STORE, 0, st));
+    QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{const_cast<double*>(Ci), nb, nb, nb},
+                    D + w2 * nb, w2, nb, nb, nb, GEMM_EPI_SUB, 0, st));
+    g_launches += 2;
+  }
+  h->rinv2_ready = true;
+  return QRB_OK;
+}
+
+// B (n x nrhs) <- R^-1 B, bottom-up: panel pairs as 2nb blocks (inverse block +
+// rank-2nb update, K = 2nb GEMMs), single nb blocks where no full pair exists
+int trsm_upper_h(qrb_handle* h, const MatView& B, cudaStream_t st) {
+  const int nb = h->nb;
+  const int64_t n = h->n, nrhs = B.cols;
+  if (n <= 0 || nrhs <= 0) return QRB_OK;
+  ProfScope ps(QRB_K_TRSM, static_cast<double>(n) * n * nrhs,
+               8.0 * (0.5 * n * (double)n + 2.0 * n * (double)nrhs), st);
+  MatView R{h->A, n, n, h->lda};
+  const int64_t w2 = 2 * int64_t(nb);
+  for (int k = h->npanels - 1; k >= 0;) {
+    const bool pair = (k & 1) && pair_ok(h, k - 1);
+    const int kb = pair ? k - 1 : k;
+    const int64_t i0 = int64_t(kb) * nb;
+    const int64_t bs = pair ? w2 : std::min<int64_t>(nb, n - i0);
+    MatView Yk = B.sub(i0, 0, bs, nrhs);
+    if (pair) {
+      // Y_k <- D Y_k through a copy (M = 2nb spans two row tiles: no in-place GEMM)
+      const int64_t ldt = w2;
+      QRB_TRY(h->Ytmp.ensure(sizeof(double) * ldt * nrhs, st));
+      QRB_CUDA_TRY(cudaMemcpy2DAsync(h->Ytmp.d(), sizeof(double) * ldt, Yk.ptr,
+                                     sizeof(double) * Yk.ld, sizeof(double) * bs, nrhs,
+                                     cudaMemcpyDeviceToDevice, st));
+      QRB_TRY(gemm_nn(MatView{h->Rinv2 + int64_t(kb / 2) * w2 * w2, bs, bs, w2},
+                      MatView{h->Ytmp.d(), bs, nrhs, ldt}, Yk.ptr, Yk.ld, bs, nrhs, bs,
+                      GEMM_EPI_STORE, 0, st));
+    } else {
+      MatView Ri{h->Rinv + int64_t(kb) * nb * nb, bs, bs, nb};
+      QRB_TRY(gemm_nn(Ri, Yk, Yk.ptr, Yk.ld, bs, nrhs, bs, GEMM_EPI_STORE, 0, st));
+    }
+    g_launches += 1;
+    if (i0 > 0) {
+      MatView Rk = R.sub(0, i0, i0, bs);
+      QRB_TRY(gemm_nn(Rk, Yk, B.ptr, B.ld, i0, nrhs, bs, GEMM_EPI_SUB, 0, st));
+      g_launches += 1;
+    }
+    k = kb - 1;
+  }
   return QRB_OK;
 }
 
@@ -655,6 +791,9 @@ int qrb_destroy(qrb_handle* h) {
   if (h->tau) cudaFree(h->tau);
   if (h->T) cudaFree(h->T);
   if (h->Rinv) cudaFree(h->Rinv);
+  if (h->T2) cudaFree(h->T2);
+  if (h->Rinv2) cudaFree(h->Rinv2);
+  h->Ytmp.release();
   h->Bw.release();
   h->resid.release();
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -694,6 +833,8 @@ int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->factored = false;
   h->rinv_ready = false;
+  h->t2_ready = false;
+  h->rinv2_ready = false;
   return QRB_OK;
 }
 
@@ -788,6 +929,8 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   }
   h->factored = true;
   h->rinv_ready = false;
+  h->t2_ready = false;
+  h->rinv2_ready = false;
   session.finish(rep);
   if (rep) {
     const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
@@ -924,6 +1067,8 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     QRB_CUDA_TRY(cudaMemcpy(&hflag, nf, sizeof(int), cudaMemcpyDeviceToHost));
     h->factored = hflag == 0;
     h->rinv_ready = false;
+  h->t2_ready = false;
+  h->rinv2_ready = false;
     if (hflag) {
       set_last_error("factorize: input matrix has non-finite entries");
       status = QRB_ENONFINITE;
@@ -967,6 +1112,8 @@ int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t l
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->factored = true;
   h->rinv_ready = false;
+  h->t2_ready = false;
+  h->rinv2_ready = false;
   return QRB_OK;
 }
 
@@ -1014,14 +1161,23 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
   QRB_TRY(ensure_rinv(h));
+  QRB_TRY(ensure_t2(h, ws));
   MatView A{h->A, h->m, h->n, h->lda};
   MatView Bv{Bw, h->m, nrhs, ldw};
-  for (int k = 0; k < h->npanels; ++k) {
+  for (int k = 0; k < h->npanels;) {
     const int64_t j0 = int64_t(k) * h->nb;
     const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
     const int64_t mk = h->m - j0;
+    if (pair_ok(h, k)) {  // two panels at once with the merged reflector (K = 2nb)
+      const int64_t w2 = 2 * int64_t(h->nb);
+      QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), h->T2 + int64_t(k / 2) * w2 * w2, w2,
+                       Bv.sub(j0, 0, mk, nrhs), ws, st));
+      k += 2;
+      continue;
+    }
     QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), h->T + int64_t(k) * h->nb * h->nb, h->nb,
                      Bv.sub(j0, 0, mk, nrhs), ws, st));
+    ++k;
   }
   if (resid) {
     QRB_TRY(h->resid.ensure(sizeof(double) * nrhs, st));
@@ -1029,7 +1185,12 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
                          static_cast<int>(nrhs), h->resid.d(), st));
     g_launches += 1;
   }
-  QRB_TRY(trsm_upper(A.sub(0, 0, h->n, h->n), h->Rinv, h->nb, Bv.sub(0, 0, h->n, nrhs), st));
+  if (g_outer_panels == 2) {
+    QRB_TRY(ensure_rinv2(h));
+    QRB_TRY(trsm_upper_h(h, Bv.sub(0, 0, h->n, nrhs), st));
+  } else {
+    QRB_TRY(trsm_upper(A.sub(0, 0, h->n, h->n), h->Rinv, h->nb, Bv.sub(0, 0, h->n, nrhs), st));
+  }
   QRB_CUDA_TRY(cudaEventRecord(h->ev2, st));
   QRB_CUDA_TRY(cudaMemcpy2DAsync(X, ldx * sizeof(double), Bw, ldw * sizeof(double),
                                  h->n * sizeof(double), nrhs,
