@@ -44,6 +44,7 @@ constexpr int SD_THREADS = 512;
 constexpr int NP = 128;
 
 struct SdBuf {
+  int series;          // G = I + F with ||F|| <= 1e-8: first-order closed form
   double row[2][NP];   // row k of the working matrix (f operands)
   double mul[2][NP];   // masked multipliers
   double piv[NP];
@@ -141,6 +142,11 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
     double tot = 0.0;
     for (int w = 0; w < SD_THREADS / 32; ++w) tot += sb.red[w];
     if (check_identity && !(tot <= 0.25)) sb.bad = 1;
+    // second CholeskyQR pass on a well-conditioned panel: G = I + F with tiny F.
+    // chol(I + F) = I + U + O(||F||^2), (I + U)^-1 = I - U + O(||F||^2) with
+    // U = strict_upper(F) + diag(F)/2, so below 1e-8 both are exact to rounding
+    // and the 128-step sweep is skipped.
+    sb.series = check_identity && tot <= 1e-16;
     double d = sb.row[0][0];
     if (!(d > 0.0 && d < INFINITY)) {
       sb.bad = 1;
@@ -150,6 +156,20 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
     sb.rec[0] = frcp(d);
   }
   __syncthreads();
+  if (sb.series) {
+    if (c < b) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int i = g + 4 * q;
+        if (i < b) {
+          const double u = i < c ? x[q] : (i == c ? 0.5 * (x[q] - 1.0) : 0.0);
+          R[i + (int64_t)c * ldo] = (i == c ? 1.0 : 0.0) + u;
+          Rinv[i + (int64_t)c * ldo] = (i == c ? 1.0 : 0.0) - u;
+        }
+      }
+    }
+    return;  // bad is 0 here (the identity check passed)
+  }
   for (int k = 0; k < NP; ++k) {
     const double rk = sb.rec[k];
     const double* mul = sb.mul[k & 1];       // S(k, i) for i > k, else 0

@@ -120,3 +120,24 @@ def test_factorize_and_solve_with_cholqr2_panels(native, algo):
     assert np.abs(x_gpu - x_ref).max() <= 1e-8 * np.abs(x_ref).max()
     res_ref = np.linalg.norm(a @ x_ref - b, axis=0)
     np.testing.assert_allclose(res_gpu, res_ref, rtol=1e-9)
+
+
+def test_cholqr2_moderately_conditioned_panel_takes_the_full_second_pass(native):
+    """cond ~1e5: ||Q1^T Q1 - I|| ~ 1e-6 is above the closed-form threshold, so
+    the second Cholesky runs as a full sweep -- still the Householder factors."""
+    nat, lib = native
+    rng = np.random.default_rng(21)
+    m, w = 9000, 128
+    u, _ = np.linalg.qr(rng.standard_normal((m, w)))
+    v, _ = np.linalg.qr(rng.standard_normal((w, w)))
+    a = (u * np.logspace(0, -5, w)) @ v.T
+    f0 = nat.get_tuning("cholqr_fallbacks")
+    p2, tau2, t2 = _panel(lib, a, 2, nat)
+    assert nat.get_tuning("cholqr_fallbacks") == f0
+    p1, tau1, t1 = _panel(lib, a, 1, nat)
+    r1, r2 = np.triu(p1[:w]), np.triu(p2[:w])
+    assert np.abs(r2 - r1).max() <= 1e-9 * np.abs(r1).max()
+    assert np.abs(tau2 - tau1).max() <= 1e-9
+    v2 = np.tril(p2, -1) + np.eye(m, w)
+    q = np.eye(m) - v2 @ np.triu(t2) @ v2.T
+    assert np.linalg.norm(q.T @ q - np.eye(m)) <= 1e-12
