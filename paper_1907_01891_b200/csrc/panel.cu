@@ -389,6 +389,60 @@ __global__ void trtri_blocks_kernel(const double* A, int64_t lda, int n, int bs,
   }
 }
 
+// Inverses of the 2nb x 2nb diagonal blocks of R for the panel pairs, one CTA
+// per pair, from the nb-block inverses:
+//   [[A, B], [0, C]]^-1 = [[A^-1, -A^-1 B C^-1], [0, C^-1]]
+// (one launch for all pairs instead of two small GEMM launches per pair).
+// Block p covers rows/cols [p*2nb, (p+1)*2nb) of R; Rinv holds the nb-block
+// inverses (nb x nb each, packed); out gets 2nb x 2nb blocks (ld 2nb).
+constexpr int RI2_THREADS = 512;
+__global__ void __launch_bounds__(RI2_THREADS) rinv2_kernel(const double* R, int64_t ldr,
+                                                            const double* Rinv, int nb,
+                                                            double* out) {
+  extern __shared__ double zs[];  // Z = A^-1 B, nb x nb, ld nb + 1
+  const int p = blockIdx.x;
+  const int64_t j0 = (int64_t)p * 2 * nb;
+  const double* Ai = Rinv + (int64_t)(2 * p) * nb * nb;
+  const double* Ci = Ai + (int64_t)nb * nb;
+  const double* Bb = R + j0 + (j0 + nb) * ldr;  // R[j0:j0+nb, j0+nb:j0+2nb]
+  const int w2 = 2 * nb, L = nb + 1;
+  double* D = out + (int64_t)p * w2 * w2;
+  const int t = threadIdx.x;
+  const int cg = t / nb, r = t - cg * nb;      // row r, column group cg
+  const int ngroups = RI2_THREADS / nb;        // 4 for nb = 128
+  // phase 1: Z[r][c] = sum_{l >= r} A^-1[r][l] B[l][c]
+  if (cg < ngroups) {
+    for (int c0 = cg; c0 < nb; c0 += ngroups * 8) {
+      double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int l = r; l < nb; ++l) {
+        const double a = Ai[r + (int64_t)l * nb];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u * ngroups;
+          if (c < nb) z[u] += a * __ldg(Bb + l + (int64_t)c * ldr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * ngroups;
+        if (c < nb) zs[r + c * L] = z[u];
+      }
+    }
+  }
+  __syncthreads();
+  // phase 2: D12[r][c] = -sum_{l <= c} Z[r][l] C^-1[l][c]; the diagonal blocks copied
+  if (cg < ngroups) {
+    for (int c = cg; c < nb; c += ngroups) {
+      double acc = 0.0;
+      for (int l = 0; l <= c; ++l) acc += zs[r + l * L] * __ldg(Ci + l + (int64_t)c * nb);
+      D[r + (int64_t)(nb + c) * w2] = -acc;
+      D[r + (int64_t)c * w2] = Ai[r + (int64_t)c * nb];
+      D[nb + r + (int64_t)(nb + c) * w2] = Ci[r + (int64_t)c * nb];
+      D[nb + r + (int64_t)c * w2] = 0.0;
+    }
+  }
+}
+
 // per-column sum of squares of rows [r0, r1) of a column-major matrix
 __global__ void column_sumsq_kernel(const double* B, int64_t ldb, int r0, int r1, double* out) {
   const int col = blockIdx.x;
@@ -561,6 +615,20 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
   int blocks = static_cast<int>(std::min<int64_t>((total + 127) / 128, 8 * 148));
   reduce_splits_kernel<<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols, ldp,
                                                    out, ldo);
+  QRB_CUDA_TRY(cudaGetLastError());
+  return QRB_OK;
+}
+
+int rinv2_pairs(const double* R, int64_t ldr, const double* Rinv, int nb, int npairs, double* out,
+                cudaStream_t stream) {
+  if (npairs <= 0) return QRB_OK;
+  if (nb < 1 || nb > 128 || RI2_THREADS % nb) {
+    set_last_error("rinv2_pairs: nb must divide 512 and be <= 128");
+    return QRB_ERR_ARG;
+  }
+  const size_t smem = (size_t)nb * (nb + 1) * sizeof(double);
+  QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(rinv2_kernel), smem));
+  rinv2_kernel<<<npairs, RI2_THREADS, smem, stream>>>(R, ldr, Rinv, nb, out);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
 }

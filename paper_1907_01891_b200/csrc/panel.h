@@ -28,6 +28,11 @@ int build_t(const double* G, int ldg, const double* tau, int w, double* T, int l
 int reduce_splits(const double* parts, int64_t split_stride, int splits, int rows, int cols,
                   int64_t ldp, double* out, int64_t ldo, cudaStream_t stream);
 
+// inverses of the 2nb x 2nb diagonal blocks of R (pairs p of nb blocks) from the
+// packed nb-block inverses, one launch; out: npairs blocks of 2nb x 2nb (ld 2nb)
+int rinv2_pairs(const double* R, int64_t ldr, const double* Rinv, int nb, int npairs, double* out,
+                cudaStream_t stream);
+
 int trtri_blocks(const double* A, int64_t lda, int n, int bs, double* Rinv, cudaStream_t stream);
 
 int axpy_block(double alpha, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t rows,

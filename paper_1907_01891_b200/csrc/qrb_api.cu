@@ -439,7 +439,8 @@ static int merge_pair_t(const MatView& A, int64_t j0, int nb, const double* Ta, 
 }
 
 static int factor_panel_pair(const MatView& A, int64_t j0, int nb, double* Ta, double* Tb,
-                             double* tau, double** T2out, Workspace& ws, cudaStream_t st) {
+                             double* tau, double** T2out, Workspace& ws, cudaStream_t st,
+                             double* T2dst = nullptr) {
   const int64_t mk = A.rows - j0;
   const int w2 = 2 * nb;
   const MatView Va = A.sub(j0, j0, mk, nb);
@@ -448,8 +449,9 @@ static int factor_panel_pair(const MatView& A, int64_t j0, int nb, double* Ta, d
   const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, nb);
   QRB_TRY(factor_panel(Vb, tau + j0 + nb, Tb, nb, ws, st));
   QRB_TRY(ws.T2.ensure(sizeof(double) * (int64_t(w2) * w2 + 3 * int64_t(nb) * nb), st));
-  QRB_TRY(merge_pair_t(A, j0, nb, Ta, Tb, ws.T2.d(), w2, ws.T2.d() + int64_t(w2) * w2, ws, st));
-  *T2out = ws.T2.d();
+  double* dst = T2dst ? T2dst : ws.T2.d();
+  QRB_TRY(merge_pair_t(A, j0, nb, Ta, Tb, dst, w2, ws.T2.d() + int64_t(w2) * w2, ws, st));
+  *T2out = dst;
   return QRB_OK;
 }
 
@@ -521,8 +523,9 @@ struct qrb_handle {
   double* Rinv = nullptr;  // npanels blocks of nb x nb
   bool factored = false;
   bool rinv_ready = false;
-  double* T2 = nullptr;    // merged 2nb x 2nb reflectors of panel pairs (solve), lazily
-  bool t2_ready = false;
+  double* T2 = nullptr;    // merged 2nb x 2nb reflectors of panel pairs (kept from the
+  bool t2_ready = false;   //   factorization's pair steps, the rest filled at the first solve)
+  std::vector<char> t2_valid;
   double* Rinv2 = nullptr; // inverses of the 2nb x 2nb diagonal blocks of R (pairs), lazily
   bool rinv2_ready = false;
   DevBuf Ytmp;             // copy of a 2nb-row block of the right-hand sides
@@ -595,6 +598,23 @@ bool pair_ok(const qrb_handle* h, int k) {
          h->m - j0 >= 2 * int64_t(h->nb);
 }
 
+// storage of the merged pair reflectors (npairs blocks of 2nb x 2nb + scratch)
+int t2_storage(qrb_handle* h) {
+  const int64_t w2 = 2 * int64_t(h->nb), blk = w2 * w2;
+  const int npairs = h->npanels / 2;
+  if (!h->T2 && npairs > 0) {
+    if (cudaMalloc(&h->T2, sizeof(double) * (npairs * blk + 2 * int64_t(h->nb) * h->nb)) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      h->T2 = nullptr;
+      set_last_error("T2 alloc failed");
+      return QRB_ENOMEM;
+    }
+  }
+  h->t2_valid.assign(npairs, 0);
+  return QRB_OK;
+}
+
 int ensure_t2(qrb_handle* h, Workspace& ws) {
   if (h->t2_ready) return QRB_OK;
   const int nb = h->nb;
@@ -604,21 +624,15 @@ int ensure_t2(qrb_handle* h, Workspace& ws) {
     h->t2_ready = true;
     return QRB_OK;
   }
-  if (!h->T2) {
-    if (cudaMalloc(&h->T2, sizeof(double) * (npairs * blk + 2 * int64_t(nb) * nb)) != cudaSuccess) {
-      cudaGetLastError();
-      h->T2 = nullptr;
-      set_last_error("qrb_solve: T2 alloc failed");
-      return QRB_ENOMEM;
-    }
-  }
+  if (!h->T2 || static_cast<int>(h->t2_valid.size()) != npairs) QRB_TRY(t2_storage(h));
   MatView A{h->A, h->m, h->n, h->lda};
   double* scratch = h->T2 + npairs * blk;
   for (int p = 0; p < npairs; ++p) {
-    if (!pair_ok(h, 2 * p)) continue;
+    if (!pair_ok(h, 2 * p) || h->t2_valid[p]) continue;
     const double* Ta = h->T + int64_t(2 * p) * nb * nb;
     QRB_TRY(merge_pair_t(A, int64_t(2 * p) * nb, nb, Ta, Ta + int64_t(nb) * nb, h->T2 + p * blk,
                          w2, scratch, ws, h->stream));
+    h->t2_valid[p] = 1;
   }
   h->t2_ready = true;
   return QRB_OK;
@@ -652,28 +666,11 @@ int ensure_rinv2(qrb_handle* h) {
       return QRB_ENOMEM;
     }
   }
-  cudaStream_t st = h->stream;
-  double* Z = h->Rinv2 + npairs * blk;
-  for (int p = 0; p < npairs; ++p) {
-    const int k = 2 * p;
-    if (!pair_ok(h, k)) continue;
-    const int64_t j0 = int64_t(k) * nb;
-    double* D = h->Rinv2 + p * blk;
-    const double* Ai = h->Rinv + int64_t(k) * nb2;
-    const double* Ci = Ai + nb2;
-    QRB_CUDA_TRY(cudaMemset2DAsync(D, sizeof(double) * w2, 0, sizeof(double) * w2, w2, st));
-    QRB_CUDA_TRY(cudaMemcpy2DAsync(D, sizeof(double) * w2, Ai, sizeof(double) * nb,
-                                   sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
-    QRB_CUDA_TRY(cudaMemcpy2DAsync(D + nb + w2 * nb, sizeof(double) * w2, Ci, sizeof(double) * nb,
-                                   sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
-    // Z = A^-1 B, B = R[j0:j0+nb, j0+nb:j0+2nb];  D12 = -Z C^-1
-    const MatView Bblk{h->A + j0 + (j0 + nb) * h->lda, nb, nb, h->lda};
-    QRB_TRY(gemm_nn(MatView{const_cast<double*>(Ai), nb, nb, nb}, Bblk, Z, nb, nb, nb, nb,
-                    GEMM_EPI_STORE, 0, st));
-    QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{const_cast<double*>(Ci), nb, nb, nb},
-                    D + w2 * nb, w2, nb, nb, nb, GEMM_EPI_SUB, 0, st));
-    g_launches += 2;
-  }
+  // every pair's diagonal block is inverted (pairs that the solve does not use --
+  // a partial last panel -- are simply never read)
+  const int full_pairs = static_cast<int>(std::min<int64_t>(npairs, h->n / w2));
+  QRB_TRY(rinv2_pairs(h->A, h->lda, h->Rinv, nb, full_pairs, h->Rinv2, h->stream));
+  g_launches += 1;
   h->rinv2_ready = true;
   return QRB_OK;
 }
@@ -886,6 +883,7 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
     cudaEventCreate(&ep1);
     cudaEventCreate(&ep2);
   }
+  QRB_TRY(t2_storage(h));
   QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
   MatView A{h->A, h->m, h->n, h->lda};
   for (int k = 0; k < h->npanels; ++k) {
@@ -897,8 +895,10 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
         mk >= 2 * int64_t(h->nb)) {
       // a pair of full panels, then one trailing update with K = 2nb
       double* T2 = nullptr;
+      const int64_t blk2 = 4 * int64_t(h->nb) * h->nb;
       QRB_TRY(factor_panel_pair(A, j0, h->nb, Tk, Tk + int64_t(h->nb) * h->nb, h->tau, &T2, ws,
-                                st));
+                                st, h->T2 + (k / 2) * blk2));
+      h->t2_valid[k / 2] = 1;
       const int64_t c0 = j0 + 2 * h->nb;
       QRB_TRY(apply_qt(A.sub(j0, j0, mk, 2 * h->nb), T2, 2 * h->nb, A.sub(j0, c0, mk, h->n - c0),
                        ws, st));
@@ -997,6 +997,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     cudaEventRecord(c1ev, cs);
     ProfSession session(h);
     MatView A{h->A, h->m, h->n, h->lda};
+    QRB_TRY(t2_storage(h));
     // non-finite input check per landed chunk (flag read once at the end)
     QRB_TRY(ws.bar.ensure(64, st));
     int* nf = static_cast<int*>(ws.bar.p) + 8;
@@ -1023,7 +1024,11 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
           double* Tk = h->T + (j0 / nb) * nb * nb;
           if (g_outer_panels == 2 && j0 + 2 * int64_t(nb) < h->n && mk >= 2 * int64_t(nb)) {
             double* T2 = nullptr;
-            status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st);
+            const int64_t kp = j0 / nb;
+            const bool keep = (kp & 1) == 0;
+            status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
+                                       keep ? h->T2 + (kp / 2) * 4 * int64_t(nb) * nb : nullptr);
+            if (keep && status == QRB_OK) h->t2_valid[kp / 2] = 1;
             if (status == QRB_OK)
               status = apply_qt(A.sub(j0, j0, mk, 2 * nb), T2, 2 * nb,
                                 A.sub(j0, j0 + 2 * nb, mk, h->n - j0 - 2 * nb), ws, st);
