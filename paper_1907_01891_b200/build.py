@@ -20,7 +20,7 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libqrb200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["gemm_dmma.cu", "panel.cu", "cholqr.cu", "siddon.cu", "qrb_api.cu"]
+SOURCES = ["gemm_dmma.cu", "panel.cu", "cholqr.cu", "smallfact.cu", "siddon.cu", "qrb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

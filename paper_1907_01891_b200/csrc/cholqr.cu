@@ -25,6 +25,8 @@
 #include "cholqr.h"
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace qrb {
 
 namespace {
@@ -388,12 +390,15 @@ size_t sd_smem(int) { return (size_t)NP * (NP + 1) * sizeof(double); }
 
 }  // namespace
 
+static const bool g_sweep_legacy = std::getenv("QRB_SWEEP_LEGACY") != nullptr;
+
 int chol_inv(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, int* flag, int bit,
              int check_identity, cudaStream_t stream) {
   if (b < 1 || b > 128) {
     set_last_error("chol_inv: b must be in [1, 128]");
     return QRB_ERR_ARG;
   }
+  if (!g_sweep_legacy) return chol_inv_blk(G, ldg, b, R, Rinv, ldo, flag, bit, check_identity, stream);
   chol_inv_kernel<<<1, SD_THREADS, 0, stream>>>(G, ldg, b, R, Rinv, ldo, flag, bit,
                                                           check_identity);
   QRB_CUDA_TRY(cudaGetLastError());
@@ -407,6 +412,8 @@ int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, doub
     set_last_error("modified_lu: b must be in [1, 128]");
     return QRB_ERR_ARG;
   }
+  if (!g_sweep_legacy)
+    return modified_lu_blk(Qt, ldq, b, Uc, NUcS, L1, Ucinv, L1invT, s, ldo, flag, bit, stream);
   QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(tri_inv_kernel), sd_smem(128)));
   mlu_kernel<<<1, SD_THREADS, 0, stream>>>(Qt, ldq, b, Uc, NUcS, L1, s, ldo, flag, bit);
   QRB_CUDA_TRY(cudaGetLastError());

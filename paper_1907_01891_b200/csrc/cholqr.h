@@ -16,6 +16,14 @@ int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, doub
                 double* Ucinv, double* L1invT, double* s, int ldo, int* flag, int bit,
                 cudaStream_t stream);
 
+// blocked shared-memory versions of the two above (smallfact.cu); chol_inv /
+// modified_lu dispatch to them unless QRB_SWEEP_LEGACY is set
+int chol_inv_blk(const double* G, int ldg, int b, double* R, double* Rinv, int ldo, int* flag,
+                 int bit, int check_identity, cudaStream_t stream);
+int modified_lu_blk(const double* Qt, int ldq, int b, double* Uc, double* NUcS, double* L1,
+                    double* Ucinv, double* L1invT, double* s, int ldo, int* flag, int bit,
+                    cudaStream_t stream);
+
 // P[0:b,0:b] <- diag(s) R on/above the diagonal, L1 below; tau_k = T_kk.
 int cholqr_write_top(double* P, int64_t ldp, int b, const double* R, const double* s,
                      const double* L1, const double* T, int64_t ldt, double* tau, int ldo,
