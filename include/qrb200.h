@@ -70,6 +70,7 @@ typedef struct qrb_kernel_stat {
 #define QRB_K_GEMM_TT 2 /* W2 = T^T W                                          */
 #define QRB_K_GEMM_NN 3 /* C -= V W2 (DMMA)                                    */
 #define QRB_K_TRSM 4    /* back substitution                                    */
+#define QRB_K_GEMM_NN_CAP 5 /* C -= V W2 on a capped grid beside the look-ahead panel */
 #define QRB_K_COUNT 8
 
 typedef struct qrb_report {
@@ -226,6 +227,13 @@ QRB_API int qrb_release_workspace(void);
  *                      uses the merged 2nb-wide block reflector (K = 2nb GEMMs); 1: one by one
  *   "nn_dynamic"       1: the persistent trailing-update GEMM hands out tiles dynamically
  *                      (for multi-GPU runs, where NCCL kernels may hold SMs); 0: static
+ *   "lookahead"        1 (default): while the trailing update of panel pair s runs on
+ *                      capped GEMM grids, pair s+1 is factored on a second (high-priority)
+ *                      stream on the remaining SMs; 0: serial; 3: only when the update
+ *                      outlasts the modelled panel time.  Results are bitwise identical.
+ *   "la_sms"           SMs left to the look-ahead panel (default 24)
+ *   "la_lat_us", "la_margin_pct"  panel-time model sizing the capped part of the update
+ *   "la_steps"         (read only) steps that ran with look-ahead
  *   "cholqr_panels"    (read only) panels that tried the CholeskyQR2 route
  *   "cholqr_fallbacks" (read only) of those, panels that fell back to Householder columns
  * qrb_set_tuning returns QRB_ERR_ARG for an unknown or read-only key. */

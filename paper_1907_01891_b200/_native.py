@@ -29,7 +29,7 @@ QRB_ESTATE = -5
 QRB_EUNSUPPORTED = -6
 
 
-KERNEL_NAMES = ("panel", "gemm_tn", "gemm_tt", "gemm_nn", "trsm", "k5", "k6", "k7")
+KERNEL_NAMES = ("panel", "gemm_tn", "gemm_tt", "gemm_nn", "trsm", "gemm_nn_capped", "k6", "k7")
 
 
 class QrbKernelStat(ctypes.Structure):

@@ -28,4 +28,15 @@ void gemm_set_nn_dynamic(bool on);
 bool gemm_nn_dynamic();
 int gemm_sm_count();
 
+// Upper bound on the CTAs of the GEMMs launched by this host thread (0 = no
+// cap): a capped launch runs persistent on that many SMs, leaving the rest to
+// work on another stream (the look-ahead panel of qrb_factorize).
+void gemm_set_grid_cap(int cap);
+int gemm_grid_cap();
+struct GemmGridCap {
+  int old;
+  explicit GemmGridCap(int cap) : old(gemm_grid_cap()) { gemm_set_grid_cap(cap); }
+  ~GemmGridCap() { gemm_set_grid_cap(old); }
+};
+
 }  // namespace qrb

@@ -46,7 +46,7 @@ constexpr int THREADS = (CONSUMER_WARPS + 1) * 32;
 
 struct GemmArgs {
   int M, N, K;
-  int k_per_split;
+  int k_per_split, nsplit;
   double* out;
   int64_t ldo;
   int64_t split_stride;
@@ -137,20 +137,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // tile rasterization: groups of group_m M-tiles sweep the N-tiles together
+  // work units = (output tile, K split); CTAs stride over them (a capped grid
+  // makes the kernel persistent, e.g. to leave SMs to a concurrent panel)
   const int num_m = (args.M + BM - 1) / BM;
   const int num_n = (args.N + BN - 1) / BN;
-  const int tile = blockIdx.x;
-  const int per_group = args.group_m * num_n;
-  const int first_m = (tile / per_group) * args.group_m;
-  const int gsize = min(num_m - first_m, args.group_m);
-  const int local = tile % per_group;
-  const int m_tile = first_m + local % gsize;
-  const int n_tile = local / gsize;
-
-  const int k_begin = blockIdx.z * args.k_per_split;
-  const int k_end = min(args.K, k_begin + args.k_per_split);
-  const int num_k = (k_end - k_begin + BK - 1) / BK;
+  const int tiles = num_m * num_n;
+  const int units = tiles * args.nsplit;
+  auto decode = [&](int u, int& m_tile, int& n_tile, int& split) {
+    split = u / tiles;
+    const int tile = u - split * tiles;
+    const int per_group = args.group_m * num_n;
+    const int first_m = (tile / per_group) * args.group_m;
+    const int gsize = min(num_m - first_m, args.group_m);
+    const int local = tile % per_group;
+    m_tile = first_m + local % gsize;
+    n_tile = local / gsize;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -163,24 +165,32 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == CONSUMER_WARPS) {
     // ---------------- producer warp: TMA ----------------
-    if (lane == 0 && num_k > 0) {
+    if (lane == 0) {
       prefetch_tmap(&mapA);
       prefetch_tmap(&mapB);
-      for (int kt = 0; kt < num_k; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
-        uint8_t* sA = smem + s * STAGE_BYTES;
-        uint8_t* sB = sA + A_BYTES;
-        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        const int k = k_begin + kt * BK;
-        if constexpr (A_KMAJOR) {
-          tma_load_2d(sA, &mapA, k, m_tile * BM, &full[s]);
-        } else {
+      int kit = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m_tile, n_tile, split;
+        decode(u, m_tile, n_tile, split);
+        const int k_begin = split * args.k_per_split;
+        const int k_end = min(args.K, k_begin + args.k_per_split);
+        const int num_k = (k_end - k_begin + BK - 1) / BK;
+        for (int kt = 0; kt < num_k; ++kt, ++kit) {
+          const int s = kit % STAGES;
+          if (kit >= STAGES) mbar_wait(&empty[s], ((kit / STAGES) & 1) ^ 1);
+          uint8_t* sA = smem + s * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const int k = k_begin + kt * BK;
+          if constexpr (A_KMAJOR) {
+            tma_load_2d(sA, &mapA, k, m_tile * BM, &full[s]);
+          } else {
 #pragma unroll
-          for (int mb = 0; mb < BM / 16; ++mb)
-            tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+            for (int mb = 0; mb < BM / 16; ++mb)
+              tma_load_2d(sA + mb * 2048, &mapA, m_tile * BM + mb * 16, k, &full[s]);
+          }
+          tma_load_2d(sB, &mapB, k, n_tile * BN, &full[s]);
         }
-        tma_load_2d(sB, &mapB, k, n_tile * BN, &full[s]);
       }
     }
     return;
@@ -191,93 +201,101 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (BN / 2);
-  const int mg0 = m_tile * BM;
-  const int ng0 = n_tile * BN;
+  int kit = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int m_tile, n_tile, split;
+    decode(u, m_tile, n_tile, split);
+    const int k_begin = split * args.k_per_split;
+    const int k_end = min(args.K, k_begin + args.k_per_split);
+    const int num_k = (k_end - k_begin + BK - 1) / BK;
+    const int mg0 = m_tile * BM;
+    const int ng0 = n_tile * BN;
 
-  double acc[4][NT][2];
+    double acc[4][NT][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < num_k; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const uint8_t* sA = smem + s * STAGE_BYTES;
-    const uint8_t* sB = sA + A_BYTES;
-    const int kg0 = k_begin + kt * BK;
-    bool ma = false, mb = false;
-    if (args.mask_a) {
-      ma = A_KMAJOR ? (kg0 <= mg0 + BM - 1) : (mg0 <= kg0 + BK - 1);
+    for (int kt = 0; kt < num_k; ++kt, ++kit) {
+      const int s = kit % STAGES;
+      mbar_wait(&full[s], (kit / STAGES) & 1);
+      const uint8_t* sA = smem + s * STAGE_BYTES;
+      const uint8_t* sB = sA + A_BYTES;
+      const int kg0 = k_begin + kt * BK;
+      bool ma = false, mb = false;
+      if (args.mask_a) {
+        ma = A_KMAJOR ? (kg0 <= mg0 + BM - 1) : (mg0 <= kg0 + BK - 1);
+      }
+      if (args.mask_b) mb = (kg0 <= ng0 + BN - 1);
+      if (ma || mb) {
+        if (ma && mb)
+          consume_stage<A_KMAJOR, BN, true, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+        else if (ma)
+          consume_stage<A_KMAJOR, BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+        else
+          consume_stage<A_KMAJOR, BN, false, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      } else {
+        consume_stage<A_KMAJOR, BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (args.mask_b) mb = (kg0 <= ng0 + BN - 1);
-    if (ma || mb) {
-      if (ma && mb)
-        consume_stage<A_KMAJOR, BN, true, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
-      else if (ma)
-        consume_stage<A_KMAJOR, BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
-      else
-        consume_stage<A_KMAJOR, BN, false, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
-    } else {
-      consume_stage<A_KMAJOR, BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
 
-  // ---------------- epilogue ----------------
-  double* out = args.out + static_cast<int64_t>(blockIdx.z) * args.split_stride;
-  const int64_t ldo = args.ldo;
-  if constexpr (A_KMAJOR) {
+    // ---------------- epilogue ----------------
+    double* out = args.out + static_cast<int64_t>(split) * args.split_stride;
+    const int64_t ldo = args.ldo;
+    if constexpr (A_KMAJOR) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int m = mg0 + m0 + mt * 8 + rp(g);
-      if (m >= args.M) continue;
+      for (int mt = 0; mt < 4; ++mt) {
+        const int m = mg0 + m0 + mt * 8 + rp(g);
+        if (m >= args.M) continue;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
-          if (n < args.N) {
-            double* p = out + m + static_cast<int64_t>(n) * ldo;
-            if constexpr (EPI == GEMM_EPI_SUB)
-              *p -= acc[mt][nt][e];
-            else
-              *p = acc[mt][nt][e];
+          for (int e = 0; e < 2; ++e) {
+            const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
+            if (n < args.N) {
+              double* p = out + m + static_cast<int64_t>(n) * ldo;
+              if constexpr (EPI == GEMM_EPI_SUB)
+                *p -= acc[mt][nt][e];
+              else
+                *p = acc[mt][nt][e];
+            }
           }
         }
       }
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int mp = 0; mp < 2; ++mp) {
-      const int m = mg0 + m0 + mp * 16 + 2 * g;
-      if (m >= args.M) continue;
-      const bool pair = (m + 1 < args.M);
+      for (int mp = 0; mp < 2; ++mp) {
+        const int m = mg0 + m0 + mp * 16 + 2 * g;
+        if (m >= args.M) continue;
+        const bool pair = (m + 1 < args.M);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+        for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
-          if (n >= args.N) continue;
-          double* p = out + m + static_cast<int64_t>(n) * ldo;
-          const double v0 = acc[mp * 2 + 0][nt][e];
-          const double v1 = acc[mp * 2 + 1][nt][e];
-          if (pair) {
-            double2* p2 = reinterpret_cast<double2*>(p);
-            if constexpr (EPI == GEMM_EPI_SUB) {
-              double2 c = *p2;
-              c.x -= v0;
-              c.y -= v1;
-              *p2 = c;
+          for (int e = 0; e < 2; ++e) {
+            const int n = ng0 + n0 + nt * 8 + rp(2 * q + e);
+            if (n >= args.N) continue;
+            double* p = out + m + static_cast<int64_t>(n) * ldo;
+            const double v0 = acc[mp * 2 + 0][nt][e];
+            const double v1 = acc[mp * 2 + 1][nt][e];
+            if (pair) {
+              double2* p2 = reinterpret_cast<double2*>(p);
+              if constexpr (EPI == GEMM_EPI_SUB) {
+                double2 c = *p2;
+                c.x -= v0;
+                c.y -= v1;
+                *p2 = c;
+              } else {
+                *p2 = make_double2(v0, v1);
+              }
             } else {
-              *p2 = make_double2(v0, v1);
+              if constexpr (EPI == GEMM_EPI_SUB)
+                *p -= v0;
+              else
+                *p = v0;
             }
-          } else {
-            if constexpr (EPI == GEMM_EPI_SUB)
-              *p -= v0;
-            else
-              *p = v0;
           }
         }
       }
@@ -993,13 +1011,20 @@ int launch(const MatView& a, const MatView& b, double* out, int64_t ldo, int64_t
   const int num_n = (N + BN - 1) / BN;
   const int nsplit = (K + kps - 1) / kps;
   if (used) *used = nsplit;
-  dim3 grid(num_m * num_n, 1, nsplit);
+  args.nsplit = nsplit;
+  const int units = num_m * num_n * nsplit;
+  const int cap = gemm_grid_cap();
+  const int grid = cap > 0 ? std::min(units, cap) : units;
   gemm_dmma_kernel<A_KMAJOR, BN, EPI><<<grid, THREADS, SMEM, stream>>>(ma, mb, args);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
 }
 
 }  // namespace
+
+static thread_local int t_grid_cap = 0;
+void gemm_set_grid_cap(int cap) { t_grid_cap = cap; }
+int gemm_grid_cap() { return t_grid_cap; }
 
 int gemm_sm_count() {
   static int sms = 0;
@@ -1079,7 +1104,8 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     const int num_m = (M + BM - 1) / BM;
     const int num_n = (N + NN_BN - 1) / NN_BN;
     args.num_tiles = num_m * num_n;
-    const int grid = std::min(args.num_tiles, gemm_sm_count());
+    const int cap = gemm_grid_cap();
+    const int grid = std::min(args.num_tiles, cap > 0 ? std::min(cap, gemm_sm_count()) : gemm_sm_count());
     if (!dyn) {
       gemm_nn_sub_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
       QRB_CUDA_TRY(cudaGetLastError());

@@ -168,15 +168,23 @@ static Workspace& device_workspace() {
   return ws[dev & 63];
 }
 
+// buffers of the look-ahead panel, which runs on a second stream concurrently
+// with the trailing update that uses device_workspace()
+static Workspace& side_workspace() {
+  static Workspace ws[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return ws[dev & 63];
+}
+
 static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 
-// C <- (I - V T^T V^T) C   i.e. C <- Q^T C,  V m x w unit lower (in place under R)
-static int apply_qt(const MatView& V, const double* T, int64_t ldt, const MatView& C,
-                    Workspace& ws, cudaStream_t st) {
+// W2 = T^T (V^T C) into ws.W2 (w x nc, ld even(w)); V m x w unit lower (in place under R)
+static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const MatView& C,
+                       Workspace& ws, cudaStream_t st) {
   const int m = static_cast<int>(V.rows);
   const int w = static_cast<int>(V.cols);
   const int nc = static_cast<int>(C.cols);
-  if (nc <= 0 || w <= 0 || m <= 0) return QRB_OK;
   const int64_t ldw = even(w);
   QRB_TRY(ws.W.ensure(sizeof(double) * ldw * nc, st));
   QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));
@@ -206,14 +214,32 @@ static int apply_qt(const MatView& V, const double* T, int64_t ldt, const MatVie
                  8.0 * (2.0 * w * nc + (double)w * w), st);
     QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
   }
-  // C -= V W2
-  MatView W2v{ws.W2.d(), w, nc, ldw};
-  {
-    ProfScope ps(QRB_K_GEMM_NN, fl, 8.0 * (2.0 * m * nc + (double)m * w + (double)w * nc), st);
-    QRB_TRY(gemm_nn(V, W2v, C.ptr, C.ld, m, nc, w, GEMM_EPI_SUB, 1, st));
-  }
-  g_launches += 2;
+  g_launches += 1;
   return QRB_OK;
+}
+
+// C[:, c_from : c_from + cols] -= V W2[:, c_from : ...]   (W2 from apply_qt_w2 over C)
+static int apply_qt_nn(const MatView& V, const MatView& C, int64_t c_from, int64_t cols,
+                       Workspace& ws, cudaStream_t st, int kind = QRB_K_GEMM_NN) {
+  if (cols <= 0) return QRB_OK;
+  const int m = static_cast<int>(V.rows);
+  const int w = static_cast<int>(V.cols);
+  const int64_t ldw = even(w);
+  const double fl = 2.0 * m * static_cast<double>(cols) * w;
+  MatView W2v{ws.W2.d() + c_from * ldw, w, cols, ldw};
+  ProfScope ps(kind, fl, 8.0 * (2.0 * m * cols + (double)m * w + (double)w * cols), st);
+  QRB_TRY(gemm_nn(V, W2v, C.ptr + c_from * C.ld, C.ld, m, static_cast<int>(cols), w,
+                  GEMM_EPI_SUB, 1, st));
+  g_launches += 1;
+  return QRB_OK;
+}
+
+// C <- (I - V T^T V^T) C   i.e. C <- Q^T C,  V m x w unit lower (in place under R)
+static int apply_qt(const MatView& V, const double* T, int64_t ldt, const MatView& C,
+                    Workspace& ws, cudaStream_t st) {
+  if (C.cols <= 0 || V.cols <= 0 || V.rows <= 0) return QRB_OK;
+  QRB_TRY(apply_qt_w2(V, T, ldt, C, ws, st));
+  return apply_qt_nn(V, C, 0, C.cols, ws, st);
 }
 
 // Householder QR of an m x w panel (w <= 128) in place, tau[w], T (w x w, ldt)
@@ -536,6 +562,9 @@ struct qrb_handle {
   DevBuf resid;
   bool profiling = false;
   Profiler prof;
+  cudaStream_t side = nullptr;                // look-ahead panel stream (high priority)
+  cudaEvent_t ev_upd = nullptr, ev_pan = nullptr;
+  DevBuf T2scratch;                           // merged reflectors of pairs not kept in T2
 };
 
 namespace {
@@ -718,6 +747,128 @@ int trsm_upper_h(qrb_handle* h, const MatView& B, cudaStream_t st) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// right-looking steps from column col0 to the end, panel pairs with look-ahead
+//
+// Step s (pair at j0, merged reflector V, T2; trailing columns c0 = j0 + 2nb ..):
+//   main stream:  C[:, c0 : c0+2nb] <- Q^T C   (the next pair's columns, all SMs)
+//                 C[:, c0+2nb : c_cap] <- Q^T C  (GEMM grids capped to sms - R)
+//                 C[:, c_cap : n]  <- Q^T C      (all SMs)
+//   side stream:  (after the first update) factor the next pair on the R free
+//                 SMs -- the panel's latency-bound chain (small factorizations,
+//                 launch gaps, host flag check) runs under the big update.
+// c_cap is a deterministic function of the shape (a model of the panel time on
+// R SMs), so the rounding of every column is the same run to run.  With too
+// little trailing work left the step runs serially (panel, then update).
+// ---------------------------------------------------------------------------
+static int g_lookahead = [] {
+  const char* e = std::getenv("QRB_LOOKAHEAD");
+  return e ? std::atoi(e) : 1;
+}();
+static int g_la_sms = 24;              // SMs left to the look-ahead panel (r01 sweep: 8..48)
+static int64_t g_la_lat_us = 250;      // latency part of a pair's panel chain (r01 sweep)
+static int64_t g_la_margin_pct = 25;   // capped window = (1 + margin) x modelled panel time
+static std::atomic<int64_t> g_la_steps{0};
+
+static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_t st) {
+  const int nb = h->nb;
+  const int64_t m = h->m, n = h->n, w2 = 2 * int64_t(nb), blk2 = w2 * w2;
+  MatView A{h->A, m, n, h->lda};
+  auto pair_here = [&](int64_t j0) { return g_outer_panels == 2 && j0 + w2 < n && m - j0 >= w2; };
+  // merged reflector storage: pairs starting at an even panel are kept for the
+  // solve (h->T2); others alternate between two scratch slots
+  auto t2dst = [&](int64_t j0) -> double* {
+    const int64_t kp = j0 / nb;
+    if ((kp & 1) == 0) return h->T2 + (kp / 2) * blk2;
+    return h->T2scratch.d() + ((j0 / w2) & 1) * blk2;
+  };
+  auto t2mark = [&](int64_t j0) {
+    const int64_t kp = j0 / nb;
+    if ((kp & 1) == 0) h->t2_valid[kp / 2] = 1;
+  };
+  QRB_TRY(h->T2scratch.ensure(sizeof(double) * 2 * blk2, st));
+  const int sms = gemm_sm_count();
+  const int R = std::min(g_la_sms, sms / 2);
+  if (g_lookahead && !h->side) {
+    int lo = 0, hi = 0;
+    QRB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    QRB_CUDA_TRY(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
+    QRB_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_upd, cudaEventDisableTiming));
+    QRB_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pan, cudaEventDisableTiming));
+  }
+  const double rate = 34.0e9;  // flop per ms of the DMMA update on all SMs (r01 bench)
+  double* T2 = nullptr;
+  bool have_pair = false;  // the pair at j0 was factored by the previous step's look-ahead
+  int64_t j0 = col0;
+  while (j0 < n) {
+    const int64_t mk = m - j0;
+    double* Tk = h->T + (j0 / nb) * nb * int64_t(nb);
+    if (!pair_here(j0)) {
+      const int64_t pw = std::min<int64_t>(nb, n - j0);
+      QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st));
+      if (j0 + pw < n)
+        QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, n - j0 - pw), ws,
+                         st));
+      j0 += pw;
+      have_pair = false;
+      continue;
+    }
+    if (!have_pair) {
+      QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
+                                t2dst(j0)));
+      t2mark(j0);
+    }
+    have_pair = false;
+    const int64_t c0 = j0 + w2, rest = n - c0;
+    const MatView V = A.sub(j0, j0, mk, w2);
+    bool la = g_lookahead && h->side && pair_here(c0);
+    int64_t ncap = 0;
+    if (la) {
+      // modelled chain time of the next pair on R SMs: latency part + its GEMM
+      // flops (2 Gram + 2 NN per panel, Q_a^T on panel b, the T merge ~ 26 m nb^2)
+      const double mk1 = static_cast<double>(m - c0);
+      const double tp = g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * R / sms);
+      const double capped_rate = rate * (sms - R) / sms;
+      const double per_col = 2.0 * static_cast<double>(mk) * w2;  // NN flops per column
+      const double want = (1.0 + g_la_margin_pct / 100.0) * tp * capped_rate / per_col;
+      ncap = std::min<int64_t>(rest - w2, (static_cast<int64_t>(want) + 63) / 64 * 64);
+      // lookahead = 1: always (even a short update hides part of the panel:
+      // r01 sweep, config 2 27.5 -> 28.8 TFLOP/s against skipping short steps);
+      // lookahead = 3: only when the remaining NN update outlasts the panel chain
+      if (g_lookahead == 3) la = (rest - w2) * per_col / capped_rate > tp;
+    }
+    if (!la) {
+      QRB_TRY(apply_qt(V, T2, w2, A.sub(j0, c0, mk, rest), ws, st));
+      j0 = c0;
+      continue;
+    }
+    ++g_la_steps;
+    // W2 for every trailing column in one TN pass (same split-K as the serial
+    // schedule: bitwise-identical results), then the NN update in three parts
+    const MatView C = A.sub(j0, c0, mk, rest);
+    QRB_TRY(apply_qt_w2(V, T2, w2, C, ws, st));
+    QRB_TRY(apply_qt_nn(V, C, 0, w2, ws, st));
+    QRB_CUDA_TRY(cudaEventRecord(h->ev_upd, st));
+    {
+      GemmGridCap cap(sms - R);
+      QRB_TRY(apply_qt_nn(V, C, w2, ncap, ws, st, QRB_K_GEMM_NN_CAP));
+    }
+    QRB_TRY(apply_qt_nn(V, C, w2 + ncap, rest - w2 - ncap, ws, st));
+    // the next pair on the side stream (its host-side flag check blocks this
+    // thread only while the update above is already queued on the GPU)
+    QRB_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_upd, 0));
+    double* Tn = h->T + (c0 / nb) * nb * int64_t(nb);
+    QRB_TRY(factor_panel_pair(A, c0, nb, Tn, Tn + int64_t(nb) * nb, h->tau, &T2, side_workspace(),
+                              h->side, t2dst(c0)));
+    t2mark(c0);
+    QRB_CUDA_TRY(cudaEventRecord(h->ev_pan, h->side));
+    QRB_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_pan, 0));
+    have_pair = true;
+    j0 = c0;
+  }
+  return QRB_OK;
+}
+
 extern "C" {
 
 int qrb_version(void) { return 100; }
@@ -796,6 +947,13 @@ int qrb_destroy(qrb_handle* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev2) cudaEventDestroy(h->ev2);
+  if (h->side) {
+    cudaStreamSynchronize(h->side);
+    cudaStreamDestroy(h->side);
+  }
+  if (h->ev_upd) cudaEventDestroy(h->ev_upd);
+  if (h->ev_pan) cudaEventDestroy(h->ev_pan);
+  h->T2scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return QRB_OK;
@@ -886,33 +1044,20 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   QRB_TRY(t2_storage(h));
   QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
   MatView A{h->A, h->m, h->n, h->lda};
-  for (int k = 0; k < h->npanels; ++k) {
-    const int64_t j0 = int64_t(k) * h->nb;
-    const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
-    const int64_t mk = h->m - j0;
-    double* Tk = h->T + int64_t(k) * h->nb * h->nb;
-    if (g_outer_panels == 2 && !timing && j0 + 2 * int64_t(h->nb) < h->n &&
-        mk >= 2 * int64_t(h->nb)) {
-      // a pair of full panels, then one trailing update with K = 2nb
-      double* T2 = nullptr;
-      const int64_t blk2 = 4 * int64_t(h->nb) * h->nb;
-      QRB_TRY(factor_panel_pair(A, j0, h->nb, Tk, Tk + int64_t(h->nb) * h->nb, h->tau, &T2, ws,
-                                st, h->T2 + (k / 2) * blk2));
-      h->t2_valid[k / 2] = 1;
-      const int64_t c0 = j0 + 2 * h->nb;
-      QRB_TRY(apply_qt(A.sub(j0, j0, mk, 2 * h->nb), T2, 2 * h->nb, A.sub(j0, c0, mk, h->n - c0),
-                       ws, st));
-      ++k;
-      continue;
-    }
-    if (timing) cudaEventRecord(ep0, st);
-    QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, h->nb, ws, st));
-    if (timing) cudaEventRecord(ep1, st);
-    if (j0 + pw < h->n) {
-      QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, h->nb, A.sub(j0, j0 + pw, mk, h->n - j0 - pw),
-                       ws, st));
-    }
-    if (timing) {
+  if (!timing) {
+    QRB_TRY(right_looking(h, 0, ws, st));
+  } else {
+    for (int k = 0; k < h->npanels; ++k) {  // serial, single panels, per-phase events
+      const int64_t j0 = int64_t(k) * h->nb;
+      const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
+      const int64_t mk = h->m - j0;
+      double* Tk = h->T + int64_t(k) * h->nb * h->nb;
+      cudaEventRecord(ep0, st);
+      QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, h->nb, ws, st));
+      cudaEventRecord(ep1, st);
+      if (j0 + pw < h->n)
+        QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, h->nb,
+                         A.sub(j0, j0 + pw, mk, h->n - j0 - pw), ws, st));
       cudaEventRecord(ep2, st);
       cudaEventSynchronize(ep2);
       panel_ms += elapsed(ep0, ep1);
@@ -1019,27 +1164,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
           status = apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
                             A.sub(j0, col0, mk, rem), ws, st);
         }
-        for (int64_t j0 = col0; j0 < h->n && status == QRB_OK; j0 += nb) {
-          const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
-          double* Tk = h->T + (j0 / nb) * nb * nb;
-          if (g_outer_panels == 2 && j0 + 2 * int64_t(nb) < h->n && mk >= 2 * int64_t(nb)) {
-            double* T2 = nullptr;
-            const int64_t kp = j0 / nb;
-            const bool keep = (kp & 1) == 0;
-            status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
-                                       keep ? h->T2 + (kp / 2) * 4 * int64_t(nb) * nb : nullptr);
-            if (keep && status == QRB_OK) h->t2_valid[kp / 2] = 1;
-            if (status == QRB_OK)
-              status = apply_qt(A.sub(j0, j0, mk, 2 * nb), T2, 2 * nb,
-                                A.sub(j0, j0 + 2 * nb, mk, h->n - j0 - 2 * nb), ws, st);
-            j0 += nb;
-            continue;
-          }
-          status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
-          if (status == QRB_OK && j0 + pw < h->n)
-            status = apply_qt(A.sub(j0, j0, mk, pw), Tk, nb,
-                              A.sub(j0, j0 + pw, mk, h->n - j0 - pw), ws, st);
-        }
+        if (status == QRB_OK) status = right_looking(h, col0, ws, st);
         break;
       }
       QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[c], 0));
@@ -1384,6 +1509,7 @@ int qrb_copy_2d(double* dst, int64_t ldd, const double* src, int64_t lds, int64_
 int qrb_release_workspace(void) {
   cudaDeviceSynchronize();
   device_workspace().release();
+  side_workspace().release();
   return QRB_OK;
 }
 
@@ -1407,6 +1533,22 @@ int qrb_set_tuning(const char* key, int64_t value) {
     gemm_set_nn_dynamic(value == 1);
     return QRB_OK;
   }
+  if (k == "lookahead" && value >= 0 && value <= 3) {
+    g_lookahead = static_cast<int>(value);
+    return QRB_OK;
+  }
+  if (k == "la_sms" && value >= 1 && value <= 100) {
+    g_la_sms = static_cast<int>(value);
+    return QRB_OK;
+  }
+  if (k == "la_lat_us" && value >= 0) {
+    g_la_lat_us = value;
+    return QRB_OK;
+  }
+  if (k == "la_margin_pct" && value >= 0 && value <= 1000) {
+    g_la_margin_pct = value;
+    return QRB_OK;
+  }
   set_last_error("qrb_set_tuning: unknown key or bad value: " + k);
   return QRB_ERR_ARG;
 }
@@ -1421,6 +1563,11 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "cholqr_min_rows") *value = g_cholqr_min_rows;
   else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
   else if (k == "outer_panels") *value = g_outer_panels;
+  else if (k == "lookahead") *value = g_lookahead;
+  else if (k == "la_sms") *value = g_la_sms;
+  else if (k == "la_lat_us") *value = g_la_lat_us;
+  else if (k == "la_margin_pct") *value = g_la_margin_pct;
+  else if (k == "la_steps") *value = g_la_steps.load();
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
   else if (k == "cholqr_fallbacks") *value = g_cholqr_fallbacks.load();
   else {
