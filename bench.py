@@ -286,6 +286,8 @@ def ours_arm(args, rank: int, world: int):
                                  "frac_of_its_sms": ca / (FP64_PEAK_TFLOPS * (sms - la_sms) / sms),
                                  "launches": ck["launches"], "ms": ck["ms"]}
     shares = {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4) for k, v in kstats.items()}
+    roofline["kernel_tflops"] = {k: round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 3)
+                                 for k, v in kstats.items() if v["ms"] > 0 and k.startswith("gemm")}
 
     # residual sanity of the last step: GPU residual identity vs explicit ||Ax - b||
     x_last = x_dev[:, :n]
@@ -410,25 +412,27 @@ def emit(line: dict) -> None:
 
 
 def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
-    """DRAM bytes of the dominant kernel from the committed `ncu --set full`
-    capture (profiles/r01_ncu_full_gemm_nn_config3.txt: the k = 0 launch of the
-    config-3 NN update C -= V W2, C = m x (n - nb), V = m x nb, W2 = nb x (n - nb)).
-    Read from the committed summary, not measured in this run."""
-    prof = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_gemm_nn_config3.txt"
+    """DRAM bytes of the dominant kernel's launch from the committed `ncu --set
+    full` capture (profiles/r01_ncu_full_gemm_nn_k256_config3.txt: the longest
+    NN launch of the first config-3 pair step, C -= V W2 with the shape in its
+    launch_shape line).  Read from the committed summary, not measured in this run."""
+    prof = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_gemm_nn_k256_config3.txt"
     if kernel != "gemm_nn" or (m, n) != (69120, 65536) or not prof.is_file():
         return {}
-    vals = {}
+    vals, shape = {}, None
     for line in prof.read_text().splitlines():
         parts = line.split(",")
         if len(parts) >= 2 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             vals[parts[0]] = float(parts[1]) * 1e9
-    if len(vals) != 2:
+        if parts[0] == "launch_shape":
+            shape = tuple(int(x) for x in parts[1:4])
+    if len(vals) != 2 or shape is None:
         return {}
-    nc = n - nb
-    algo = 8.0 * (2 * m * nc + m * nb + nb * nc)
+    mm, nc, k = shape
+    algo = 8.0 * (2 * mm * nc + mm * k + k * nc)  # C read + write, V, W2
     return {"traffic": sum(vals.values()), "traffic_unit": "bytes",
-            "traffic_launch": f"k=0 launch ({m}x{nc}x{nb}), ncu --set full, "
-                              "profiles/r01_ncu_full_gemm_nn_config3.txt",
+            "traffic_launch": f"one launch {mm}x{nc}x{k} (ncu --set full, "
+                              "profiles/r01_ncu_full_gemm_nn_k256_config3.txt)",
             "traffic_algorithmic": algo}
 
 
