@@ -169,6 +169,27 @@ QRB_API int qrb_op_panel(double* panel, int64_t ldp, int64_t m, int64_t w, doubl
 QRB_API int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
                     int64_t ldt, double* C, int64_t ldc, int64_t nc, void* stream);
 
+/* Householder QR of an m x w block (w <= 2 nb) in place, as two panels: the
+ * first nb columns, Q_a^T applied to the rest, the remaining w - nb columns;
+ * per-panel T factors in T (two nb x nb column-major blocks, ld nb) and the
+ * merged w x w block reflector T2 = [[T_a, -T_a V_a^T V_b T_b], [0, T_b]]
+ * (ld ldt2).  side != 0 uses a second library workspace, so the call may run
+ * on another stream concurrently with qrb_op_apply_qt_*.  One step of the
+ * multi-GPU factorization (dist.py; comp_dense_qr, kernels.py:296-321, for a
+ * 2nb-wide tile column). */
+QRB_API int qrb_op_panel_block(double* A, int64_t lda, int64_t m, int64_t w, int nb, double* tau,
+                               double* T, double* T2, int64_t ldt2, void* stream, int side);
+
+/* qrb_op_apply_qt in two phases: _begin forms W2 = T^T V^T C for all nc
+ * columns (kept in the library workspace), _cols then applies C -= V W2 to
+ * columns [c_from, c_from + ncols) -- so a look-ahead panel can start after the
+ * first columns while the rest is updated (on a capped grid, "grid_cap"). */
+QRB_API int qrb_op_apply_qt_begin(const double* V, int64_t ldv, int64_t m, int64_t w,
+                                  const double* T, int64_t ldt, const double* C, int64_t ldc,
+                                  int64_t nc, void* stream);
+QRB_API int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, double* C,
+                                 int64_t ldc, int64_t c_from, int64_t ncols, void* stream);
+
 /* Reference-format interop: [F; G] <- Q^T [F; G] for a triangle-on-dense tile
  * factorization produced by the reference (D = b x b reflector tile, S = its
  * packed T tile with inner width w, F / G = b x nc blocks).  Replaces
@@ -234,6 +255,8 @@ QRB_API int qrb_release_workspace(void);
  *   "la_sms"           SMs left to the look-ahead panel (default 24)
  *   "la_lat_us", "la_margin_pct"  panel-time model sizing the capped part of the update
  *   "la_steps"         (read only) steps that ran with look-ahead
+ *   "grid_cap"         CTAs of the GEMMs launched by the calling host thread (0 = no cap)
+ *   "sm_count"         (read only) SMs of the current device
  *   "cholqr_panels"    (read only) panels that tried the CholeskyQR2 route
  *   "cholqr_fallbacks" (read only) of those, panels that fell back to Householder columns
  * qrb_set_tuning returns QRB_ERR_ARG for an unknown or read-only key. */

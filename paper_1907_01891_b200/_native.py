@@ -13,7 +13,8 @@ from pathlib import Path
 
 from .errors import NativeUnavailableError
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqrb200.so"
+_LIB_PATH = Path(os.environ.get("QRB_LIB_PATH") or
+                 Path(__file__).resolve().parent / "_lib" / "libqrb200.so")  # override: A/B builds
 
 c_int = ctypes.c_int
 c_i64 = ctypes.c_int64
@@ -84,6 +85,12 @@ SIGNATURES = {
     "qrb_op_panel": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_void_p, c_i64, c_void_p]),
     "qrb_op_apply_qt": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_void_p, c_i64,
                                 c_i64, c_void_p]),
+    "qrb_op_panel_block": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_int, c_void_p, c_void_p,
+                                   c_void_p, c_i64, c_void_p, c_int]),
+    "qrb_op_apply_qt_begin": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_void_p,
+                                      c_i64, c_i64, c_void_p]),
+    "qrb_op_apply_qt_cols": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_i64, c_i64,
+                                     c_void_p]),
     "qrb_op_apply_qt_td": (c_int, [c_void_p, c_i64, c_i64, c_i64, c_void_p, c_i64, c_void_p,
                                    c_i64, c_void_p, c_i64, c_i64, c_void_p]),
     "qrb_op_gemm_nn_sub": (c_int, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_i64, c_i64,

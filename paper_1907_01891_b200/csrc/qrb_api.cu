@@ -430,36 +430,37 @@ static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ld
 // scratch: 2 nb x nb blocks
 static int merge_pair_t(const MatView& A, int64_t j0, int nb, const double* Ta, const double* Tb,
                         double* T2, int64_t ldt2, double* scratch, Workspace& ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, int wb = 0) {
+  if (wb <= 0) wb = nb;  // width of the second panel (the last block may be narrower)
   const int64_t mk = A.rows - j0;
   double* Y = scratch;
   double* Z = Y + int64_t(nb) * nb;
   const MatView Va_lo = A.sub(j0 + nb, j0, mk - nb, nb);      // plain rows of V_a
-  const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, nb);    // unit lower V_b
+  const MatView Vb = A.sub(j0 + nb, j0 + nb, mk - nb, wb);    // unit lower V_b
   const int64_t per = int64_t(nb) * nb;
-  const int splits = gemm_pick_splits(nb, nb, static_cast<int>(mk - nb), 256);
+  const int splits = gemm_pick_splits(nb, wb, static_cast<int>(mk - nb), 256);
   if (splits > 1) {
     QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
     int used = 0;
-    QRB_TRY(gemm_tn_split(Va_lo, Vb, ws.Wparts.d(), nb, per, nb, nb, static_cast<int>(mk - nb),
+    QRB_TRY(gemm_tn_split(Va_lo, Vb, ws.Wparts.d(), nb, per, nb, wb, static_cast<int>(mk - nb),
                           splits, 0, 1, st, &used));
-    QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, nb, nb, nb, Y, nb, st));
+    QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, nb, wb, nb, Y, nb, st));
     g_launches += 2;
   } else {
-    QRB_TRY(gemm_tn(Va_lo, Vb, Y, nb, 0, nb, nb, static_cast<int>(mk - nb), 1, 0, 1, st));
+    QRB_TRY(gemm_tn(Va_lo, Vb, Y, nb, 0, nb, wb, static_cast<int>(mk - nb), 1, 0, 1, st));
     g_launches += 1;
   }
-  const int w2 = 2 * nb;
+  const int w2 = nb + wb;
   QRB_CUDA_TRY(cudaMemset2DAsync(T2, sizeof(double) * ldt2, 0, sizeof(double) * w2, w2, st));
   QRB_CUDA_TRY(cudaMemcpy2DAsync(T2, sizeof(double) * ldt2, Ta, sizeof(double) * nb,
                                  sizeof(double) * nb, nb, cudaMemcpyDeviceToDevice, st));
   QRB_CUDA_TRY(cudaMemcpy2DAsync(T2 + nb + ldt2 * nb, sizeof(double) * ldt2, Tb,
-                                 sizeof(double) * nb, sizeof(double) * nb, nb,
+                                 sizeof(double) * nb, sizeof(double) * wb, wb,
                                  cudaMemcpyDeviceToDevice, st));
-  QRB_TRY(gemm_nn(MatView{const_cast<double*>(Ta), nb, nb, nb}, MatView{Y, nb, nb, nb}, Z, nb, nb,
-                  nb, nb, GEMM_EPI_STORE, 0, st));
-  QRB_TRY(gemm_nn(MatView{Z, nb, nb, nb}, MatView{const_cast<double*>(Tb), nb, nb, nb},
-                  T2 + ldt2 * nb, ldt2, nb, nb, nb, GEMM_EPI_SUB, 0, st));
+  QRB_TRY(gemm_nn(MatView{const_cast<double*>(Ta), nb, nb, nb}, MatView{Y, nb, wb, nb}, Z, nb, nb,
+                  wb, nb, GEMM_EPI_STORE, 0, st));
+  QRB_TRY(gemm_nn(MatView{Z, nb, wb, nb}, MatView{const_cast<double*>(Tb), wb, wb, nb},
+                  T2 + ldt2 * nb, ldt2, nb, wb, wb, GEMM_EPI_SUB, 0, st));
   g_launches += 2;
   return QRB_OK;
 }
@@ -1456,6 +1457,60 @@ int qrb_siddon_densify(const double* ends, int64_t n_rays, int64_t row0, int ima
                         static_cast<cudaStream_t>(stream));
 }
 
+int qrb_op_panel_block(double* A, int64_t lda, int64_t m, int64_t w, int nb, double* tau,
+                       double* T, double* T2, int64_t ldt2, void* stream, int side) {
+  if (!A || !tau || !T || !T2 || nb < 2 || nb > 128 || (nb & 1) || w < 1 || w > 2 * nb ||
+      m < w || (lda & 1) || (ldt2 & 1) || ldt2 < w) {
+    set_last_error("qrb_op_panel_block: bad arguments");
+    return QRB_EARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace& ws = side ? side_workspace() : device_workspace();
+  const MatView Av{A, m, w, lda};
+  const int64_t wa = std::min<int64_t>(w, nb), wb = w - wa;
+  QRB_TRY(factor_panel(Av.sub(0, 0, m, wa), tau, T, nb, ws, st));
+  if (wb == 0) {
+    QRB_CUDA_TRY(cudaMemset2DAsync(T2, sizeof(double) * ldt2, 0, sizeof(double) * w, w, st));
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(T2, sizeof(double) * ldt2, T, sizeof(double) * nb,
+                                   sizeof(double) * w, w, cudaMemcpyDeviceToDevice, st));
+    return QRB_OK;
+  }
+  double* Tb = T + int64_t(nb) * nb;
+  QRB_TRY(apply_qt(Av.sub(0, 0, m, nb), T, nb, Av.sub(0, nb, m, wb), ws, st));
+  QRB_TRY(factor_panel(Av.sub(nb, nb, m - nb, wb), tau + nb, Tb, nb, ws, st));
+  QRB_TRY(ws.T2.ensure(sizeof(double) * 2 * int64_t(nb) * nb, st));
+  return merge_pair_t(Av, 0, nb, T, Tb, T2, ldt2, ws.T2.d(), ws, st, static_cast<int>(wb));
+}
+
+int qrb_op_apply_qt_begin(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
+                          int64_t ldt, const double* C, int64_t ldc, int64_t nc, void* stream) {
+  if (!V || !T || !C || w < 1 || m < w || nc < 0 || (ldv & 1) || (ldc & 1) || (ldt & 1) ||
+      ldt < w) {
+    set_last_error("qrb_op_apply_qt_begin: bad arguments (leading dimensions must be even)");
+    return QRB_EARG;
+  }
+  if (nc == 0) return QRB_OK;
+  return apply_qt_w2(MatView{const_cast<double*>(V), m, w, ldv}, T, ldt,
+                     MatView{const_cast<double*>(C), m, nc, ldc}, device_workspace(),
+                     static_cast<cudaStream_t>(stream));
+}
+
+int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, double* C,
+                         int64_t ldc, int64_t c_from, int64_t ncols, void* stream) {
+  if (!V || !C || w < 1 || m < w || c_from < 0 || ncols < 0 || (ldv & 1) || (ldc & 1)) {
+    set_last_error("qrb_op_apply_qt_cols: bad arguments");
+    return QRB_EARG;
+  }
+  Workspace& ws = device_workspace();
+  if (static_cast<size_t>((c_from + ncols) * even(w)) * sizeof(double) > ws.W2.bytes) {
+    set_last_error("qrb_op_apply_qt_cols: columns beyond the last qrb_op_apply_qt_begin");
+    return QRB_EARG;
+  }
+  return apply_qt_nn(MatView{const_cast<double*>(V), m, w, ldv}, MatView{C, m, c_from + ncols, ldc},
+                     c_from, ncols, ws, static_cast<cudaStream_t>(stream),
+                     gemm_grid_cap() > 0 ? QRB_K_GEMM_NN_CAP : QRB_K_GEMM_NN);
+}
+
 int qrb_op_apply_qt_td(const double* D, int64_t ldd, int64_t b, int64_t w, const double* S,
                        int64_t lds, double* F, int64_t ldf, double* G, int64_t ldg, int64_t nc,
                        void* stream) {
@@ -1533,6 +1588,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     gemm_set_nn_dynamic(value == 1);
     return QRB_OK;
   }
+  if (k == "grid_cap" && value >= 0) {  // this host thread's GEMM grid cap (0 = none)
+    gemm_set_grid_cap(static_cast<int>(value));
+    return QRB_OK;
+  }
   if (k == "lookahead" && value >= 0 && value <= 3) {
     g_lookahead = static_cast<int>(value);
     return QRB_OK;
@@ -1564,6 +1623,8 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
   else if (k == "outer_panels") *value = g_outer_panels;
   else if (k == "lookahead") *value = g_lookahead;
+  else if (k == "grid_cap") *value = gemm_grid_cap();
+  else if (k == "sm_count") *value = gemm_sm_count();
   else if (k == "la_sms") *value = g_la_sms;
   else if (k == "la_lat_us") *value = g_la_lat_us;
   else if (k == "la_margin_pct") *value = g_la_margin_pct;

@@ -1,16 +1,22 @@
 """Multi-GPU factorization and solve: one process per GPU, torch.distributed.
 
 Layout (BASELINE.json north_star): the m x n matrix is split 1D block-cyclic
-by column panels of width nb -- panel k lives on rank k % G as local panel
-k // G, local panels stored contiguously (column-major, leading dim lda).
+by column blocks of width bw (nb, or 2 nb = a panel pair on the GPU) -- block
+k lives on rank k % G as local block k // G, local blocks stored contiguously
+(column-major, leading dim lda).
 
-Factorization, step k (j0 = k nb, m_k = m - j0):
-  1. the owner factors panel k in place (qrb_op_panel: geqr2 + T);
-  2. the owner packs (V_k, T_k) into one contiguous buffer and broadcasts it
-     (NCCL over NVLink/NVSwitch on the GPU box; gloo in the CPU tests) --
-     the single exchange of the step;
-  3. every rank applies Q_k^T to its local panels with index > k
-     (qrb_op_apply_qt: the DMMA trailing update).
+Factorization, step k (j0 = k bw, m_k = m - j0):
+  1. the owner factors block k in place (qrb_op_panel_block: one or two
+     nb-wide panels + the merged block reflector T2);
+  2. the owner packs (V_k, T2_k, tau_k) into one contiguous buffer and
+     broadcasts it (NCCL over NVLink/NVSwitch on the GPU box; gloo in the CPU
+     tests) -- the single exchange of the step;
+  3. every rank applies Q_k^T to its local blocks with index > k
+     (qrb_op_apply_qt: the DMMA trailing update, K = bw).
+With look-ahead the owner of block k+1 updates that block first, then factors
+and broadcasts it on a second stream while its own remaining update runs on
+capped GEMM grids (qrb_op_apply_qt_begin / _cols, "grid_cap") -- the
+single-GPU schedule of qrb_api.cu right_looking, per rank.
 The reference has no distributed code; its analogue of
 scaling past one device is the out-of-core tile schedule (task_engine.py:187-217).
 
@@ -39,34 +45,108 @@ def owner_of(k: int, world: int) -> int:
     return k % world
 
 
-def local_panels(npanels: int, rank: int, world: int) -> list[int]:
-    """Global indices of the panels rank owns, in local storage order."""
-    return list(range(rank, npanels, world))
+def local_panels(nblocks: int, rank: int, world: int) -> list[int]:
+    """Global indices of the column blocks rank owns, in local storage order."""
+    return list(range(rank, nblocks, world))
 
 
-def local_cols(n: int, nb: int, rank: int, world: int) -> int:
-    npan = -(-n // nb)
-    return sum(min(nb, n - k * nb) for k in local_panels(npan, rank, world))
+def local_cols(n: int, bw: int, rank: int, world: int) -> int:
+    nblk = -(-n // bw)
+    return sum(min(bw, n - k * bw) for k in local_panels(nblk, rank, world))
 
 
 def first_local_after(k: int, rank: int, world: int) -> int:
-    """Local panel index of the first owned panel with global index > k."""
+    """Local block index of the first owned block with global index > k."""
     if rank > k:
         return 0
     return (k - rank) // world + 1
+
+
+def panel_home(k: int, nb: int, bw: int, world: int) -> tuple[int, int]:
+    """(owner rank, local column) of the nb-wide panel k in a bw-block layout."""
+    j0 = k * nb
+    blk = j0 // bw
+    return owner_of(blk, world), (blk // world) * bw + (j0 - blk * bw)
 
 
 class CudaOps:
     """Local arithmetic through the C ABI (stream-ordered qrb_op_* calls on
     torch CUDA tensors holding column-major matrices as (cols, ld) tensors)."""
 
-    def __init__(self, world: int = 1):
+    def __init__(self, world: int = 1, side_lookahead: bool = True):
+        import torch
         from . import _native
         self.lib = _native.load()
         self.native = _native
         # with several ranks a receiver's NCCL kernel can hold SMs while the
         # trailing update starts: let the persistent GEMM hand out tiles dynamically
         _native.set_tuning("nn_dynamic", 1 if world > 1 else 0)
+        # the owner's next block is factored on a high-priority side stream
+        self.side_lookahead = bool(side_lookahead) and _native.get_tuning("lookahead") > 0
+        self.side = torch.cuda.Stream(priority=-1) if self.side_lookahead else None
+
+    @staticmethod
+    def _stream():
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def panel_block(self, a, lda, row0, col0, m, w, nb, tau, t2, ldt2, side=False):
+        """Block of w <= 2 nb columns at (row0, col0): V in place, tau, merged T2."""
+        import torch
+        tmp = torch.empty(2 * nb * nb, dtype=torch.float64, device=a.device)
+        st = self.lib.qrb_op_panel_block(self._p(a, row0 + col0 * lda), lda, m, w, nb, self._p(tau),
+                                         self._p(tmp), self._p(t2), ldt2, self._stream(),
+                                         1 if side else 0)
+        self.native.check(st, "qrb_op_panel_block")
+
+    def _cap_cols(self, mk, w, m_next, nb, rest):
+        """Columns of the owner's update run on the capped grid while the next
+        block is factored (the model of qrb_api.cu right_looking)."""
+        g = self.native.get_tuning
+        sms, r = g("sm_count"), g("la_sms")
+        r = min(r, sms // 2)
+        rate = 34.0e9  # flop per ms of the DMMA update on all SMs
+        tp = g("la_lat_us") * 1e-3 + 26.0 * m_next * nb * nb / (rate * r / sms)
+        want = (1.0 + g("la_margin_pct") / 100.0) * tp * rate * (sms - r) / sms / (2.0 * mk * w)
+        return min(rest, (int(want) + 63) // 64 * 64), sms - r
+
+    def apply_split(self, v, ldv, m, w, t, ldt, c, ldc, c_off, nc, first, side_work, m_next, nb):
+        """C <- Q^T C on nc columns; after the first `first` columns, side_work()
+        (the next block's factorization + broadcast) runs on the side stream
+        while the rest of the update runs on capped grids.  Returns side_work()."""
+        import torch
+        main = torch.cuda.current_stream()
+        pv, pt, pc = self._p(v), self._p(t), self._p(c, c_off)
+        first = min(first, max(nc, 0))
+        if nc > 0:
+            self.native.check(self.lib.qrb_op_apply_qt_begin(pv, ldv, m, w, pt, ldt, pc, ldc, nc,
+                                                             self._stream()), "apply_qt_begin")
+            self.native.check(self.lib.qrb_op_apply_qt_cols(pv, ldv, m, w, pc, ldc, 0, first,
+                                                            self._stream()), "apply_qt_cols")
+        ev = torch.cuda.Event()
+        ev.record(main)
+        rest = max(nc - first, 0)
+        ncap, cap = self._cap_cols(m, w, m_next, nb, rest)
+        if ncap:
+            self.native.set_tuning("grid_cap", cap)
+            try:
+                self.native.check(self.lib.qrb_op_apply_qt_cols(pv, ldv, m, w, pc, ldc, first, ncap,
+                                                                self._stream()), "apply_qt_cols")
+            finally:
+                self.native.set_tuning("grid_cap", 0)
+        if rest - ncap > 0:
+            self.native.check(self.lib.qrb_op_apply_qt_cols(pv, ldv, m, w, pc, ldc, first + ncap,
+                                                            rest - ncap, self._stream()),
+                              "apply_qt_cols")
+        # the side work is enqueued after the main stream's update: its host-side
+        # CholeskyQR2 flag check then blocks this thread with the GPU already busy
+        self.side.wait_event(ev)
+        with torch.cuda.stream(self.side):
+            res = side_work()
+            done = torch.cuda.Event()
+            done.record(self.side)
+        main.wait_event(done)
+        return res
 
     @staticmethod
     def _p(t, off=0):
@@ -114,6 +194,11 @@ class DistFactors:
     tau_all: object = None
     factor_seconds: float = 0.0
     stats: dict = field(default_factory=dict)
+    bw: int = 0                         # column block width of the layout (0 = nb)
+
+    @property
+    def block(self) -> int:
+        return self.bw or self.nb
 
 
 def _panel_views(buf, m: int, n: int, nb: int, k: int):
@@ -127,50 +212,78 @@ def _panel_views(buf, m: int, n: int, nb: int, k: int):
 
 
 def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int, world: int,
-                          ops, group=None, lookahead: bool = True) -> DistFactors:
-    """Blocked Householder QR of the block-cyclic matrix; a_local is overwritten
-    with the local panels of the factored matrix (R above, V below).
+                          ops, group=None, lookahead: bool = True, bw: int | None = None
+                          ) -> DistFactors:
+    """Blocked Householder QR of the block-cyclic matrix (blocks of bw = nb or
+    2 nb columns); a_local is overwritten with the local blocks of the factored
+    matrix (R above, V below).
 
-    With ``lookahead`` (depth 1) the owner of panel k+1 first applies Q_k^T to
-    that panel only, factors it and starts its broadcast, and only then updates
-    the rest of its trailing columns; the other ranks receive panel k+1 while
-    they are still busy with step k.  Each rank factors 1/G of the panels, so
+    With ``lookahead`` (depth 1) the owner of block k+1 first applies Q_k^T to
+    that block only, factors it and starts its broadcast, and only then updates
+    the rest of its trailing columns; the other ranks receive block k+1 while
+    they are still busy with step k.  Each rank factors 1/G of the blocks, so
     the panel latency is spread over the G GPUs instead of serialising every
-    step.  Panels travel in two alternating buffers.
+    step.  If ``ops.side_lookahead`` the owner's factorization and broadcast
+    run on a second stream concurrently with its own update (ops.apply_split).
+    Blocks travel in two alternating buffers.
     """
     import torch
     import torch.distributed as dist
 
+    bw = bw or nb
+    if bw % nb or bw > 2 * nb:
+        raise ValueError("block width must be nb or 2 nb")
+    nblk = -(-n // bw)
     npan = -(-n // nb)
     dev = a_local.device
     dt = torch.float64
     t_all = torch.zeros((npan * nb, nb), dtype=dt, device=dev)
     tau_all = torch.zeros(npan * nb, dtype=dt, device=dev)
     ldv_max = m + (m & 1)
-    bufs = [torch.empty(ldv_max * nb + nb * nb + nb, dtype=dt, device=dev) for _ in range(2)]
+    bufs = [torch.empty(ldv_max * bw + bw * bw + bw, dtype=dt, device=dev) for _ in range(2)]
     n_local = a_local.shape[0]
-    stats = {"bytes_broadcast": 0, "panels": npan, "lookahead": bool(lookahead and world > 1)}
+    side = bool(getattr(ops, "side_lookahead", False))
+    stats = {"bytes_broadcast": 0, "panels": npan, "blocks": nblk, "block_width": bw,
+             "lookahead": bool(lookahead and world > 1), "side_lookahead": side}
 
-    def factor_and_pack(k):
-        j0, pw, mk, ldv, nelem, vview, tview, tauv = _panel_views(bufs[k % 2], m, n, nb, k)
-        lcol = (k // world) * nb
-        tview.zero_()
-        ops.panel(a_local, lda, j0, lcol, mk, pw, tauv, tview, nb)
-        vview[:, :mk].copy_(a_local[lcol:lcol + pw, j0:m])
+    def views(k):
+        buf = bufs[k % 2]
+        j0 = k * bw
+        w = min(bw, n - j0)
+        mk = m - j0
+        ldv = mk + (mk & 1)
+        nelem = ldv * w + bw * bw + bw
+        return (j0, w, mk, ldv, nelem, buf[: ldv * w].view(w, ldv),
+                buf[ldv * w: ldv * w + bw * bw].view(bw, bw), buf[ldv * w + bw * bw: nelem])
+
+    def factor_and_pack(k, on_side=False):
+        j0, w, mk, ldv, nelem, vview, t2view, tauv = views(k)
+        lcol = (k // world) * bw
+        t2view.zero_()
+        ops.panel_block(a_local, lda, j0, lcol, mk, w, nb, tauv, t2view, bw, side=on_side)
+        vview[:, :mk].copy_(a_local[lcol:lcol + w, j0:m])
 
     def start_bcast(k):
-        nelem = _panel_views(bufs[k % 2], m, n, nb, k)[4]
+        nelem = views(k)[4]
         if world == 1:
             return None
         stats["bytes_broadcast"] += 8 * nelem
         return dist.broadcast(bufs[k % 2][:nelem], src=owner_of(k, world), group=group,
                               async_op=True)
 
+    def unpack(k):  # per-panel T factors (diagonal blocks of T2) and tau
+        j0, w, mk, ldv, nelem, vview, t2view, tauv = views(k)
+        for p in range(-(-w // nb)):
+            pw = min(nb, w - p * nb)
+            kp = j0 // nb + p
+            t_all[kp * nb:kp * nb + pw, :pw].copy_(t2view[p * nb:p * nb + pw, p * nb:p * nb + pw])
+        tau_all[j0:j0 + w].copy_(tauv[:w])
+
     def apply(k, col_from, col_to):
         if col_to <= col_from:
             return
-        j0, pw, mk, ldv, _, vview, tview, _ = _panel_views(bufs[k % 2], m, n, nb, k)
-        ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, a_local, lda, j0 + col_from * lda,
+        j0, w, mk, ldv, _, vview, t2view, _ = views(k)
+        ops.apply_qt(vview, ldv, 0, mk, w, t2view, bw, a_local, lda, j0 + col_from * lda,
                      col_to - col_from)
 
     la = lookahead and world > 1
@@ -183,30 +296,38 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
     if rank == owner_of(0, world):
         factor_and_pack(0)
     pending = start_bcast(0)
-    for k in range(npan):
+    for k in range(nblk):
         if pending is not None:
             pending.wait()
-        j0, pw, mk, ldv, _, vview, tview, tauv = _panel_views(bufs[k % 2], m, n, nb, k)
-        t_all[k * nb:(k + 1) * nb].copy_(tview)
-        tau_all[j0:j0 + pw].copy_(tauv[:pw])
-        lfirst = first_local_after(k, rank, world) * nb
+        unpack(k)
+        lfirst = first_local_after(k, rank, world) * bw
         nxt = k + 1
         pending = None
-        if nxt < npan and rank == owner_of(nxt, world):
-            # panel k+1 is this rank's local panel starting at lfirst
-            pw1 = min(nb, n - nxt * nb)
-            apply(k, lfirst, lfirst + pw1)
+        if nxt < nblk and rank == owner_of(nxt, world):
+            # block k+1 is this rank's local block starting at lfirst
+            w1 = min(bw, n - nxt * bw)
+            if side:
+                j0, w, mk, ldv, _, vview, t2view, _ = views(k)
+
+                def side_work(nxt=nxt):
+                    factor_and_pack(nxt, on_side=True)
+                    return start_bcast(nxt)
+                pending = ops.apply_split(vview, ldv, mk, w, t2view, bw, a_local, lda,
+                                          j0 + lfirst * lda, n_local - lfirst, w1, side_work,
+                                          m - nxt * bw, nb)
+                continue
+            apply(k, lfirst, lfirst + w1)
             factor_and_pack(nxt)
             if la:
                 pending = start_bcast(nxt)
-            apply(k, lfirst + pw1, n_local)
+            apply(k, lfirst + w1, n_local)
             if not la:
                 pending = start_bcast(nxt)
         else:
-            if la and nxt < npan:
+            if la and nxt < nblk:
                 pending = start_bcast(nxt)   # receive while updating
             apply(k, lfirst, n_local)
-            if not la and nxt < npan:
+            if not la and nxt < nblk:
                 pending = start_bcast(nxt)
     if ev is not None:
         ev[1].record()
@@ -215,7 +336,7 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
     if ev is not None:
         stats["wall_seconds"] = secs
         secs = ev[0].elapsed_time(ev[1]) / 1e3
-    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats)
+    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats, bw)
 
 
 def gather_factored(f: DistFactors, group=None, place=None):
@@ -226,7 +347,7 @@ def gather_factored(f: DistFactors, group=None, place=None):
     import torch.distributed as dist
 
     npan = -(-f.n // f.nb)
-    max_local = max(local_cols(f.n, f.nb, r, f.world) for r in range(f.world))
+    max_local = max(local_cols(f.n, f.block, r, f.world) for r in range(f.world))
     dev = f.a_local.device
     send = torch.zeros((max_local, f.lda), dtype=torch.float64, device=dev)
     send[: f.a_local.shape[0]].copy_(f.a_local)
@@ -237,9 +358,9 @@ def gather_factored(f: DistFactors, group=None, place=None):
         recv = send
     full = None if place else torch.empty((f.n, f.lda), dtype=torch.float64, device=dev)
     for k in range(npan):
-        r, lk = owner_of(k, f.world), k // f.world
+        r, lc = panel_home(k, f.nb, f.block, f.world)
         pw = min(f.nb, f.n - k * f.nb)
-        src = recv[r * max_local + lk * f.nb: r * max_local + lk * f.nb + pw]
+        src = recv[r * max_local + lc: r * max_local + lc + pw]
         if place:
             place(k, src)
         else:
@@ -270,12 +391,12 @@ def solve_distributed(f: DistFactors, b_share, ops, group=None):
     buf = torch.empty((m + (m & 1)) * nb + nb * nb + nb, dtype=torch.float64, device=dev)
     for k in range(npan):
         j0, pw, mk, ldv, nelem, vview, tview, _ = _panel_views(buf, m, n, nb, k)
-        if rank == owner_of(k, world):
-            lcol = (k // world) * nb
+        own, lcol = panel_home(k, nb, f.block, world)
+        if rank == own:
             vview[:, :mk].copy_(f.a_local[lcol:lcol + pw, j0:m])
             tview.copy_(f.t_all[k * nb:(k + 1) * nb])
         if world > 1:
-            dist.broadcast(buf[:nelem], src=owner_of(k, world), group=group)
+            dist.broadcast(buf[:nelem], src=own, group=group)
         if s:
             ops.apply_qt(vview, ldv, 0, mk, pw, tview, nb, y, lda, j0, s)
     resid = torch.linalg.norm(y[:, n:m], dim=1) if s else torch.zeros(0, device=dev)
@@ -286,11 +407,11 @@ def solve_distributed(f: DistFactors, b_share, ops, group=None):
         i1 = i0 + bs
         ldr = i1 + (i1 & 1)
         rblk = rflat[: bs * ldr].view(bs, ldr)      # R[0:i1, block k], column-major, ld = ldr
-        if rank == owner_of(k, world):
-            lcol = (k // world) * nb
+        own, lcol = panel_home(k, nb, f.block, world)
+        if rank == own:
             rblk[:, :i1].copy_(f.a_local[lcol:lcol + bs, :i1])
         if world > 1:
-            dist.broadcast(rblk, src=owner_of(k, world), group=group)
+            dist.broadcast(rblk, src=own, group=group)
         diag = torch.diagonal(rblk[:, i0:i1]).cpu().numpy()
         bad = np.flatnonzero(~(np.abs(diag) >= 1e-300))
         if bad.size:
@@ -343,11 +464,12 @@ def bench_rank(args, rank: int, world: int):
 
     g, _, x_true, S = build_workload(args.config, args.slices, host_coo=False)
     m, n, nb = g.n_rays, g.n_pixels, args.nb
+    bw = 2 * nb  # panel pairs: K = 2nb trailing-update GEMMs, one broadcast per pair
     lda = (m + 31) // 32 * 32
-    # each rank densifies only its own block-cyclic panels on its GPU
-    a_pristine = cs.densify_device(g, lda, rank=rank, world=world, nb=nb)
-    cols = [c for k in local_panels(-(-n // nb), rank, world)
-            for c in range(k * nb, min(n, (k + 1) * nb))]
+    # each rank densifies only its own block-cyclic column blocks on its GPU
+    a_pristine = cs.densify_device(g, lda, rank=rank, world=world, nb=bw)
+    cols = [c for k in local_panels(-(-n // bw), rank, world)
+            for c in range(k * bw, min(n, (k + 1) * bw))]
     xt = torch.from_numpy(np.ascontiguousarray(x_true[cols].T)).cuda()
     ax = xt @ a_pristine[:, :m]                       # this rank's share of A x
     if world > 1:
@@ -371,7 +493,7 @@ def bench_rank(args, rank: int, world: int):
 
         def reset():
             a_local.zero_()
-            cs.densify_into(g, a_local, lda, rank=rank, world=world, nb=nb)
+            cs.densify_into(g, a_local, lda, rank=rank, world=world, nb=bw)
     # replicate the factors for the solve only if a full copy (plus the gather
     # buffer) fits next to the local panels; otherwise stream V and R (config 4)
     free, total = torch.cuda.mem_get_info()
@@ -380,7 +502,7 @@ def bench_rank(args, rank: int, world: int):
 
     def step():
         reset()
-        f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
+        f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops, bw=bw)
         t1 = time.perf_counter()
         if lean:
             torch.cuda.synchronize()
@@ -432,7 +554,7 @@ def bench_rank(args, rank: int, world: int):
     torch.cuda.synchronize()
     t_e2e = time.perf_counter()
     a_local.copy_(a_pin, non_blocking=True)
-    f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops)
+    f = factorize_distributed(a_local, m, n, nb, lda, rank, world, ops, bw=bw)
     if lean:
         b_dev[:cnt].copy_(b_pin[:cnt], non_blocking=True)
         xs, _ = solve_distributed(f, b_dev[:cnt], ops)
@@ -454,8 +576,9 @@ def bench_rank(args, rank: int, world: int):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Siddon fan-beam A, seeded phantoms, 1% noise)",
             "config": {"workload": f"config{args.config}: QR of A {m}x{n} + solve {S} slices",
-                       "parallelism": f"1D block-cyclic panels nb={nb} over {world} GPUs, "
-                                      f"NCCL panel broadcast; slices split for the solve"},
+                       "parallelism": f"1D block-cyclic column blocks of {bw} (panel pairs, nb={nb}) "
+                                      f"over {world} GPUs, NCCL block broadcast, owner "
+                                      f"look-ahead on a side stream; slices split for the solve"},
             "pct_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
             "slices_per_s": S / float(s_s),
             "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,

@@ -39,6 +39,11 @@ class NumpyOps:
         tau.numpy()[:w] = taus
         strided(t, 0, w, w, ldt)[:, :] = tf
 
+    def panel_block(self, a, lda, row0, col0, m, w, nb, tau, t2, ldt2, side=False):
+        """w <= 2 nb columns as one Householder sweep: the compact-WY T of the
+        whole block equals the merged pair reflector the GPU op builds."""
+        self.panel(a, lda, row0, col0, m, w, tau, t2, ldt2)
+
     def apply_qt(self, v, ldv, v_off, m, w, t, ldt, c, ldc, c_off, nc):
         if nc <= 0:
             return
@@ -70,7 +75,7 @@ def free_port():
     return port
 
 
-def worker(rank, world, port, m, n, nb, out_dir, lookahead=True):
+def worker(rank, world, port, m, n, nb, out_dir, lookahead=True, bw=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(7)
@@ -78,10 +83,11 @@ def worker(rank, world, port, m, n, nb, out_dir, lookahead=True):
     lda = m + (m & 1)
     full = torch.zeros((n, lda), dtype=torch.float64)
     full[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T))
-    a_local = qd.scatter_block_cyclic(full, n, nb, rank, world)
-    assert a_local.shape[0] == qd.local_cols(n, nb, rank, world)
+    bw = bw or nb
+    a_local = qd.scatter_block_cyclic(full, n, bw, rank, world)
+    assert a_local.shape[0] == qd.local_cols(n, bw, rank, world)
     f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, NumpyOps(),
-                                 lookahead=lookahead)
+                                 lookahead=lookahead, bw=bw)
     fact = qd.gather_factored(f)
     if rank == 0:
         np.save(os.path.join(out_dir, "factored.npy"), fact[:, :m].numpy().T)
@@ -107,11 +113,16 @@ def worker(rank, world, port, m, n, nb, out_dir, lookahead=True):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,n,nb,la", [(2, 300, 200, 32, True), (3, 257, 250, 16, True),
-                                             (2, 64, 40, 16, True), (2, 300, 200, 32, False),
-                                             (4, 200, 150, 16, True)])
-def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb, la):
-    mp.spawn(worker, args=(world, free_port(), m, n, nb, str(tmp_path), la), nprocs=world,
+@pytest.mark.parametrize("world,m,n,nb,la,bw", [(2, 300, 200, 32, True, 32),
+                                                (3, 257, 250, 16, True, 16),
+                                                (2, 64, 40, 16, True, 16),
+                                                (2, 300, 200, 32, False, 32),
+                                                (4, 200, 150, 16, True, 16),
+                                                (2, 300, 200, 32, True, 64),
+                                                (3, 257, 250, 16, True, 32),
+                                                (2, 300, 200, 32, False, 64)])
+def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb, la, bw):
+    mp.spawn(worker, args=(world, free_port(), m, n, nb, str(tmp_path), la, bw), nprocs=world,
              join=True)
     rng = np.random.default_rng(7)
     a = rng.standard_normal((m, n))
@@ -135,6 +146,9 @@ def test_block_cyclic_factorization_matches_oracle(tmp_path, world, m, n, nb, la
 
 
 def test_ownership_helpers():
+    # panel pairs (bw = 2 nb): panel 5 is the second panel of block 2 -> rank 0 at local col 32+16
+    assert qd.panel_home(5, 16, 32, 2) == (0, 48)
+    assert qd.panel_home(2, 16, 32, 2) == (1, 0)
     assert qd.local_panels(10, 1, 4) == [1, 5, 9]
     assert qd.first_local_after(5, 1, 4) == 2   # panels 1, 5 done -> next local is 9
     assert qd.first_local_after(0, 3, 4) == 0

@@ -25,7 +25,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, m, n, nb, out_dir, lookahead):
+def _worker(rank, world, port, m, n, nb, out_dir, lookahead, bw, side):
     import torch.distributed as dist
 
     from paper_1907_01891_b200 import dist as qd
@@ -39,10 +39,10 @@ def _worker(rank, world, port, m, n, nb, out_dir, lookahead):
         lda = (m + 31) // 32 * 32
         full = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
         full[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
-        a_local = qd.scatter_block_cyclic(full, n, nb, rank, world)
-        ops = qd.CudaOps(world)
+        a_local = qd.scatter_block_cyclic(full, n, bw, rank, world)
+        ops = qd.CudaOps(world, side_lookahead=side)
         f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, ops,
-                                     lookahead=lookahead)
+                                     lookahead=lookahead, bw=bw)
         fact = qd.gather_factored(f)
         bmat = rng.standard_normal((m, 6))
         first, cnt = qd.slice_share(6, rank, world)
@@ -60,16 +60,23 @@ def _worker(rank, world, port, m, n, nb, out_dir, lookahead):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,n,nb,la", [(2, 1500, 700, 128, True), (3, 1100, 900, 64, True),
-                                             (2, 900, 500, 32, False)])
-def test_multirank_cuda_schedule_matches_oracle(tmp_path, world, m, n, nb, la):
+@pytest.mark.parametrize("world,m,n,nb,la,bw,side", [(2, 1500, 700, 128, True, 128, False),
+                                                     (3, 1100, 900, 64, True, 64, False),
+                                                     (2, 900, 500, 32, False, 32, False),
+                                                     (2, 1500, 700, 64, True, 128, True),
+                                                     (3, 1100, 900, 64, True, 128, True),
+                                                     (1, 1500, 1000, 64, True, 128, True),
+                                                     (2, 900, 500, 32, False, 64, True)])
+def test_multirank_cuda_schedule_matches_oracle(tmp_path, world, m, n, nb, la, bw, side):
+    """bw = 2 nb: panel-pair blocks (qrb_op_panel_block); side: the owner's next
+    block factored + broadcast on a side stream under its capped update."""
     import torch.multiprocessing as mp
 
     from conftest import rel_err, sign_normalise
     from oracle import tiled_qr as orc
 
-    mp.spawn(_worker, args=(world, _free_port(), m, n, nb, str(tmp_path), la), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), m, n, nb, str(tmp_path), la, bw, side),
+             nprocs=world, join=True)
     a = np.load(tmp_path / "a.npy")
     bmat = np.load(tmp_path / "b.npy")
     fact = np.load(tmp_path / "factored.npy")
