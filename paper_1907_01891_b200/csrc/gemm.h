@@ -20,6 +20,11 @@ int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ld
 int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int M, int N, int K,
             int epi, int mask_a, cudaStream_t stream);
 
+// out_z (M x N, z < splits) = Aview[:, K range z] * Bview[K range z, :] (partial products)
+int gemm_nn_split(const MatView& a_mm, const MatView& b, double* out, int64_t ldo,
+                  int64_t split_stride, int M, int N, int K, int splits, int mask_a,
+                  cudaStream_t stream, int* used);
+
 int gemm_pick_splits(int M, int N, int K, int max_splits);
 
 // dynamic tile tickets for the persistent NN update (multi-GPU runs, where an

@@ -1074,6 +1074,15 @@ int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ld
                                           mask_a, mask_b, stream, used);
 }
 
+int gemm_nn_split(const MatView& a_mm, const MatView& b, double* out, int64_t ldo,
+                  int64_t split_stride, int M, int N, int K, int splits, int mask_a,
+                  cudaStream_t stream, int* used) {
+  *used = 0;
+  if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
+  return launch<false, 64, GEMM_EPI_STORE>(a_mm, b, out, ldo, split_stride, M, N, K, splits,
+                                           mask_a, 0, stream, used);
+}
+
 static std::atomic<bool> g_nn_dynamic{false};
 void gemm_set_nn_dynamic(bool on) { g_nn_dynamic.store(on); }
 bool gemm_nn_dynamic() { return g_nn_dynamic.load(); }

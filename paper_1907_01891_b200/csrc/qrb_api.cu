@@ -179,6 +179,34 @@ static Workspace& side_workspace() {
 
 static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 
+// K splits for a product whose output has only a few 128 x 64 tiles (the solve's
+// T^T W and R_kk^-1 Y_k with 256 right-hand sides: 8 tiles on 148 SMs); a
+// function of the shape only, so results are deterministic
+static int small_splits(int M, int N, int K) {
+  const int tiles = ((M + 127) / 128) * ((N + 63) / 64);
+  int s = 1;
+  while (tiles * s * 2 <= gemm_sm_count() && K / (s * 2) >= 32 && s < 16) s *= 2;
+  return s;
+}
+
+// out (M x N) = op(A) B with few output tiles: K split over the SMs, partial
+// products summed in a fixed order by reduce_splits (out may alias B: the
+// partial GEMM reads B before the reduction writes out)
+static int small_product(bool a_kmajor, const MatView& a, const MatView& b, double* out,
+                         int64_t ldo, int M, int N, int K, int splits, Workspace& ws,
+                         cudaStream_t st) {
+  const int64_t ldp = even(M), per = ldp * N;
+  QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
+  int used = 0;
+  if (a_kmajor)
+    QRB_TRY(gemm_tn_split(a, b, ws.Wparts.d(), ldp, per, M, N, K, splits, 0, 0, st, &used));
+  else
+    QRB_TRY(gemm_nn_split(a, b, ws.Wparts.d(), ldp, per, M, N, K, splits, 0, st, &used));
+  QRB_TRY(reduce_splits(ws.Wparts.d(), per, used, M, N, ldp, out, ldo, st));
+  g_launches += 2;
+  return QRB_OK;
+}
+
 // W2 = T^T (V^T C) into ws.W2 (w x nc, ld even(w)); V m x w unit lower (in place under R)
 static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const MatView& C,
                        Workspace& ws, cudaStream_t st) {
@@ -212,9 +240,14 @@ static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const Mat
   {
     ProfScope ps(QRB_K_GEMM_TT, 2.0 * w * static_cast<double>(w) * nc,
                  8.0 * (2.0 * w * nc + (double)w * w), st);
-    QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
+    const int s2 = small_splits(w, nc, w);
+    if (s2 > 1) {
+      QRB_TRY(small_product(true, Tv, Wv, ws.W2.d(), ldw, w, nc, w, s2, ws, st));
+    } else {
+      QRB_TRY(gemm_tn(Tv, Wv, ws.W2.d(), ldw, 0, w, nc, w, 1, 0, 0, st));
+      g_launches += 1;
+    }
   }
-  g_launches += 1;
   return QRB_OK;
 }
 
@@ -721,7 +754,15 @@ int trsm_upper_h(qrb_handle* h, const MatView& B, cudaStream_t st) {
     const int64_t i0 = int64_t(kb) * nb;
     const int64_t bs = pair ? w2 : std::min<int64_t>(nb, n - i0);
     MatView Yk = B.sub(i0, 0, bs, nrhs);
-    if (pair) {
+    const int s2 = pair ? small_splits(static_cast<int>(bs), static_cast<int>(nrhs),
+                                       static_cast<int>(bs)) : 1;
+    if (pair && s2 > 1) {
+      // Y_k <- D Y_k as split-K partial products reduced into Y_k (few output tiles)
+      QRB_TRY(small_product(false, MatView{h->Rinv2 + int64_t(kb / 2) * w2 * w2, bs, bs, w2}, Yk,
+                            Yk.ptr, Yk.ld, static_cast<int>(bs), static_cast<int>(nrhs),
+                            static_cast<int>(bs), s2, device_workspace(), st));
+      g_launches -= 1;
+    } else if (pair) {
       // Y_k <- D Y_k through a copy (M = 2nb spans two row tiles: no in-place GEMM)
       const int64_t ldt = w2;
       QRB_TRY(h->Ytmp.ensure(sizeof(double) * ldt * nrhs, st));
