@@ -542,6 +542,43 @@ def bench_rank(args, rank: int, world: int):
     clocks = sampler.stop() if sampler else None
     launches = launch_count() - l0
 
+    # config 5: a 4096-slice batch on the config-3 factors, slices split over the
+    # ranks (no communication in the solve); sinograms from the all-reduced
+    # per-rank products A_local x_local
+    cfg5 = None
+    if args.config == 3 and getattr(args, "cfg5_slices", 0) > 0 and not lean:
+        S5 = args.cfg5_slices
+        x5 = cs.phantom_stack_device(5, S5)                        # (S5, n)
+        ax5 = x5[:, cols] @ a_pristine[:, :m] if a_pristine is not None else None
+        if ax5 is None:                                            # no pristine copy kept
+            reset()
+            ax5 = x5[:, cols] @ a_local[:, :m]
+        del x5
+        if world > 1:
+            dist.all_reduce(ax5)
+        f5, c5 = slice_share(S5, rank, world)
+        b5h = cs.noisy_sinograms(ax5.cpu().numpy().T, 5)           # (m, S5), same seeds as N = 1
+        del ax5
+        b5 = torch.zeros((max(c5, 1), lda), dtype=torch.float64, device="cuda")
+        b5[:c5, :m] = torch.from_numpy(np.ascontiguousarray(b5h[:, f5:f5 + c5].T)).cuda()
+        del b5h
+        x5o = torch.zeros((max(c5, 1), n + (n & 1)), dtype=torch.float64, device="cuda")
+        if c5:
+            q.solve_device(b5[:c5], x5o[:c5])                       # warm-up
+        dist.barrier()
+        t5 = []
+        for _ in range(2):
+            ms = q.solve_device(b5[:c5], x5o[:c5])["total_ms"] if c5 else 0.0
+            t5.append(ms)
+        s5 = torch.tensor([float(np.mean(t5))], device="cuda")
+        dist.all_reduce(s5, op=dist.ReduceOp.MAX)
+        cfg5 = {"workload": f"config5: solve {S5} slices on the config-3 factors, "
+                            f"{S5 // world}+ per GPU", "slices": S5, "solve_ms": float(s5),
+                "slices_per_s": S5 / (float(s5) * 1e-3),
+                "solve_tflops": solve_flops(m, n, S5) / (float(s5) * 1e-3) / 1e12}
+        del b5, x5o
+        torch.cuda.empty_cache()
+
     # end to end through host buffers: this rank's panels from pinned host memory
     # in, its slice share of X out (factorization + gather + solve inside)
     reset()
@@ -591,6 +628,7 @@ def bench_rank(args, rank: int, world: int):
                          "frac": value / world / FP64_PEAK_TFLOPS, "traffic": None,
                          "kernel": "whole factorization per GPU (CUDA events, max over "
                                    "ranks); per-kernel accounting is single-GPU only"},
+            "config5": cfg5,
             "e2e": {"value": fl / float(e2e_s) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * lda * n + 8 * m * S),
                     "d2h_bytes_per_step": int(8 * n * S),
