@@ -245,7 +245,8 @@ QRB_API int qrb_release_workspace(void);
  *   "panel_algo"       0 auto | 1 Householder columns | 2 CholeskyQR2 when the shape allows
  *   "cholqr_min_rows"  auto mode uses CholeskyQR2 for panels with at least this many rows
  *   "outer_panels"     2 (default): panels are factored in pairs and the trailing update
- *                      uses the merged 2nb-wide block reflector (K = 2nb GEMMs); 1: one by one
+ *                      uses the merged 2nb-wide block reflector (K = 2nb GEMMs); 1: one by one;
+ *                      4: two pairs merged (K = 4nb; qrb_factorize / qrb_factorize_host only)
  *   "nn_dynamic"       1: the persistent trailing-update GEMM hands out tiles dynamically
  *                      (for multi-GPU runs, where NCCL kernels may hold SMs); 0: static
  *   "lookahead"        1 (default): while the trailing update of panel pair s runs on

@@ -82,6 +82,7 @@ struct Workspace {
   DevBuf part, bar, G, Ti, W, W2, Wparts;
   DevBuf Wq, small, flag;  // CholeskyQR2 panel: Q1 (m x b), 12 b x b blocks, status word
   DevBuf T2;               // merged block reflector of a panel pair (2nb x 2nb) + scratch
+  DevBuf T4;               // scratch of the 4-panel merge (outer_panels = 4)
   int* hflag = nullptr;    // pinned host copy of the status word
   void release() {
     if (hflag) cudaFreeHost(hflag);
@@ -89,6 +90,7 @@ struct Workspace {
     Wq.release();
     small.release();
     T2.release();
+    T4.release();
     flag.release();
     part.release();
     bar.release();
@@ -452,7 +454,9 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
 // Panels per outer step (qrb_set_tuning "outer_panels": 1 or 2).
 static int g_outer_panels = [] {
   const char* e = std::getenv("QRB_OUTER_PANELS");
-  return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+  if (!e) return 2;
+  const int v = std::atoi(e);
+  return v >= 4 ? 4 : std::max(1, std::min(2, v));
 }();
 
 static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
@@ -599,6 +603,7 @@ struct qrb_handle {
   cudaStream_t side = nullptr;                // look-ahead panel stream (high priority)
   cudaEvent_t ev_upd = nullptr, ev_pan = nullptr;
   DevBuf T2scratch;                           // merged reflectors of pairs not kept in T2
+  DevBuf T4scratch;                           // merged 4nb x 4nb reflectors (outer_panels = 4)
 };
 
 namespace {
@@ -657,7 +662,7 @@ struct ProfSession {
 // merged 2nb-wide reflectors of panel pairs (2p, 2p+1), for the solve's Q^T B
 bool pair_ok(const qrb_handle* h, int k) {
   const int64_t j0 = int64_t(k) * h->nb;
-  return g_outer_panels == 2 && (k & 1) == 0 && j0 + 2 * int64_t(h->nb) <= h->n &&
+  return g_outer_panels >= 2 && (k & 1) == 0 && j0 + 2 * int64_t(h->nb) <= h->n &&
          h->m - j0 >= 2 * int64_t(h->nb);
 }
 
@@ -815,8 +820,13 @@ static std::atomic<int64_t> g_la_steps{0};
 static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_t st) {
   const int nb = h->nb;
   const int64_t m = h->m, n = h->n, w2 = 2 * int64_t(nb), blk2 = w2 * w2;
+  // outer block = q panels (2: a pair, 4: two pairs merged -> K = 4nb updates)
+  const int q = g_outer_panels >= 4 ? 4 : 2;
+  const int64_t wq = q * int64_t(nb), blkq = wq * wq;
   MatView A{h->A, m, n, h->lda};
-  auto pair_here = [&](int64_t j0) { return g_outer_panels == 2 && j0 + w2 < n && m - j0 >= w2; };
+  auto block_here = [&](int64_t j0, int64_t w) {
+    return g_outer_panels >= 2 && j0 + w < n && m - j0 >= w;
+  };
   // merged reflector storage: pairs starting at an even panel are kept for the
   // solve (h->T2); others alternate between two scratch slots
   auto t2dst = [&](int64_t j0) -> double* {
@@ -829,6 +839,33 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     if ((kp & 1) == 0) h->t2_valid[kp / 2] = 1;
   };
   QRB_TRY(h->T2scratch.ensure(sizeof(double) * 2 * blk2, st));
+  if (q == 4) QRB_TRY(h->T4scratch.ensure(sizeof(double) * 2 * blkq, st));
+  // a q-panel block at j0: pairs factored in sequence (Q_pair^T on the next
+  // pair's columns in between), merged reflector in *Tout
+  auto factor_block = [&](int64_t j0, int w, Workspace& wsb, cudaStream_t sb,
+                          double** Tout) -> int {
+    const int64_t mk = m - j0;
+    double* Tk = h->T + (j0 / nb) * nb * int64_t(nb);
+    double* T2a = nullptr;
+    QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2a, wsb, sb,
+                              t2dst(j0)));
+    t2mark(j0);
+    if (w == w2) {
+      *Tout = T2a;
+      return QRB_OK;
+    }
+    QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), T2a, w2, A.sub(j0, j0 + w2, mk, w2), wsb, sb));
+    double* Tb = Tk + 2 * int64_t(nb) * nb;
+    double* T2b = nullptr;
+    QRB_TRY(factor_panel_pair(A, j0 + w2, nb, Tb, Tb + int64_t(nb) * nb, h->tau, &T2b, wsb, sb,
+                              t2dst(j0 + w2)));
+    t2mark(j0 + w2);
+    QRB_TRY(wsb.T4.ensure(sizeof(double) * 2 * blk2, sb));
+    double* T4 = h->T4scratch.d() + ((j0 / wq) & 1) * blkq;
+    QRB_TRY(merge_pair_t(A, j0, static_cast<int>(w2), T2a, T2b, T4, wq, wsb.T4.d(), wsb, sb));
+    *Tout = T4;
+    return QRB_OK;
+  };
   const int sms = gemm_sm_count();
   const int R = std::min(g_la_sms, sms / 2);
   if (g_lookahead && !h->side) {
@@ -839,48 +876,49 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     QRB_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pan, cudaEventDisableTiming));
   }
   const double rate = 34.0e9;  // flop per ms of the DMMA update on all SMs (r01 bench)
-  double* T2 = nullptr;
-  bool have_pair = false;  // the pair at j0 was factored by the previous step's look-ahead
+  double* TB = nullptr;
+  int64_t have = 0;  // width of the block at j0 factored by the previous step's look-ahead
   int64_t j0 = col0;
   while (j0 < n) {
     const int64_t mk = m - j0;
     double* Tk = h->T + (j0 / nb) * nb * int64_t(nb);
-    if (!pair_here(j0)) {
+    const int64_t w = have ? have : (block_here(j0, wq) ? wq : block_here(j0, w2) ? w2 : 0);
+    if (w == 0) {
       const int64_t pw = std::min<int64_t>(nb, n - j0);
       QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st));
       if (j0 + pw < n)
         QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, n - j0 - pw), ws,
                          st));
       j0 += pw;
-      have_pair = false;
+      have = 0;
       continue;
     }
-    if (!have_pair) {
-      QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
-                                t2dst(j0)));
-      t2mark(j0);
-    }
-    have_pair = false;
-    const int64_t c0 = j0 + w2, rest = n - c0;
-    const MatView V = A.sub(j0, j0, mk, w2);
-    bool la = g_lookahead && h->side && pair_here(c0);
+    if (!have) QRB_TRY(factor_block(j0, static_cast<int>(w), ws, st, &TB));
+    have = 0;
+    const int64_t c0 = j0 + w, rest = n - c0;
+    const MatView V = A.sub(j0, j0, mk, w);
+    const int64_t wn = block_here(c0, wq) ? wq : block_here(c0, w2) ? w2 : 0;
+    bool la = g_lookahead && h->side && wn > 0;
     int64_t ncap = 0;
     if (la) {
-      // modelled chain time of the next pair on R SMs: latency part + its GEMM
-      // flops (2 Gram + 2 NN per panel, Q_a^T on panel b, the T merge ~ 26 m nb^2)
+      // modelled chain time of the next block on R SMs: latency part + its GEMM
+      // flops (per pair: 2 Gram + 2 NN per panel, Q_a^T on panel b, the T merge
+      // ~ 26 m nb^2; a 4-panel block ~2.3 pairs)
       const double mk1 = static_cast<double>(m - c0);
-      const double tp = g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * R / sms);
+      const double pairs = wn == w2 ? 1.0 : 2.3;
+      const double tp =
+          pairs * (g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * R / sms));
       const double capped_rate = rate * (sms - R) / sms;
-      const double per_col = 2.0 * static_cast<double>(mk) * w2;  // NN flops per column
+      const double per_col = 2.0 * static_cast<double>(mk) * w;  // NN flops per column
       const double want = (1.0 + g_la_margin_pct / 100.0) * tp * capped_rate / per_col;
-      ncap = std::min<int64_t>(rest - w2, (static_cast<int64_t>(want) + 63) / 64 * 64);
+      ncap = std::min<int64_t>(rest - wn, (static_cast<int64_t>(want) + 63) / 64 * 64);
       // lookahead = 1: always (even a short update hides part of the panel:
       // r01 sweep, config 2 27.5 -> 28.8 TFLOP/s against skipping short steps);
       // lookahead = 3: only when the remaining NN update outlasts the panel chain
-      if (g_lookahead == 3) la = (rest - w2) * per_col / capped_rate > tp;
+      if (g_lookahead == 3) la = (rest - wn) * per_col / capped_rate > tp;
     }
     if (!la) {
-      QRB_TRY(apply_qt(V, T2, w2, A.sub(j0, c0, mk, rest), ws, st));
+      QRB_TRY(apply_qt(V, TB, w, A.sub(j0, c0, mk, rest), ws, st));
       j0 = c0;
       continue;
     }
@@ -888,24 +926,21 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     // W2 for every trailing column in one TN pass (same split-K as the serial
     // schedule: bitwise-identical results), then the NN update in three parts
     const MatView C = A.sub(j0, c0, mk, rest);
-    QRB_TRY(apply_qt_w2(V, T2, w2, C, ws, st));
-    QRB_TRY(apply_qt_nn(V, C, 0, w2, ws, st));
+    QRB_TRY(apply_qt_w2(V, TB, w, C, ws, st));
+    QRB_TRY(apply_qt_nn(V, C, 0, wn, ws, st));
     QRB_CUDA_TRY(cudaEventRecord(h->ev_upd, st));
     {
       GemmGridCap cap(sms - R);
-      QRB_TRY(apply_qt_nn(V, C, w2, ncap, ws, st, QRB_K_GEMM_NN_CAP));
+      QRB_TRY(apply_qt_nn(V, C, wn, ncap, ws, st, QRB_K_GEMM_NN_CAP));
     }
-    QRB_TRY(apply_qt_nn(V, C, w2 + ncap, rest - w2 - ncap, ws, st));
-    // the next pair on the side stream (its host-side flag check blocks this
+    QRB_TRY(apply_qt_nn(V, C, wn + ncap, rest - wn - ncap, ws, st));
+    // the next block on the side stream (its host-side flag check blocks this
     // thread only while the update above is already queued on the GPU)
     QRB_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_upd, 0));
-    double* Tn = h->T + (c0 / nb) * nb * int64_t(nb);
-    QRB_TRY(factor_panel_pair(A, c0, nb, Tn, Tn + int64_t(nb) * nb, h->tau, &T2, side_workspace(),
-                              h->side, t2dst(c0)));
-    t2mark(c0);
+    QRB_TRY(factor_block(c0, static_cast<int>(wn), side_workspace(), h->side, &TB));
     QRB_CUDA_TRY(cudaEventRecord(h->ev_pan, h->side));
     QRB_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_pan, 0));
-    have_pair = true;
+    have = wn;
     j0 = c0;
   }
   return QRB_OK;
@@ -996,6 +1031,7 @@ int qrb_destroy(qrb_handle* h) {
   if (h->ev_upd) cudaEventDestroy(h->ev_upd);
   if (h->ev_pan) cudaEventDestroy(h->ev_pan);
   h->T2scratch.release();
+  h->T4scratch.release();
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return QRB_OK;
@@ -1357,7 +1393,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
                          static_cast<int>(nrhs), h->resid.d(), st));
     g_launches += 1;
   }
-  if (g_outer_panels == 2) {
+  if (g_outer_panels >= 2) {
     QRB_TRY(ensure_rinv2(h));
     QRB_TRY(trsm_upper_h(h, Bv.sub(0, 0, h->n, nrhs), st));
   } else {
@@ -1621,7 +1657,7 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_cholqr_min_rows = value;
     return QRB_OK;
   }
-  if (k == "outer_panels" && (value == 1 || value == 2)) {
+  if (k == "outer_panels" && (value == 1 || value == 2 || value == 4)) {
     g_outer_panels = static_cast<int>(value);
     return QRB_OK;
   }
