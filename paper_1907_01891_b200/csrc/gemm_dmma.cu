@@ -606,6 +606,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 // back to the DMMA main loop of the next tile (no named barrier in their path).
 // ---------------------------------------------------------------------------
 constexpr int AE_STAGES = 6;
+#ifndef QRB_NN_STAGGER_NS
+#define QRB_NN_STAGGER_NS 4000
+#endif
 constexpr int AE_SBUF = 1;  // staging buffers (the bulk read of one finishes long before the next tile)
 constexpr int AE_THREADS = (CONSUMER_WARPS + 2) * 32;  // + producer warp + epilogue warp
 constexpr int AE_SMEM = AE_STAGES * NN_STAGE_BYTES + AE_SBUF * RA_STAGING + 1024 + 256;
@@ -698,11 +701,18 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   }
 
   // ---- consumer warps: DMMA main loop, stage -acc, arrive ----
+  // Warps 4-7 start a few microseconds after warps 0-3 (which share their
+  // SMSPs) and stay behind by up to the ring depth, so the two warps of an
+  // SMSP reach the tile epilogue (staging -acc through shared memory) at
+  // different times and the DMMA pipe stays fed by the other one (tools/gemm_k.py,
+  // K = 256: 34.75 -> 34.96 TFLOP/s; flat for 4-24 us.  A barrier-enforced lag
+  // of 2-5 ring stages measured 34.34-34.43, i.e. worse).
   const int g = lane >> 2;
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (NN_BN / 2);
   int kit = 0, it = 0;
+  if (QRB_NN_STAGGER_NS > 0 && warp >= CONSUMER_WARPS / 2) __nanosleep(QRB_NN_STAGGER_NS);
   for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
     int m_tile, n_tile;
     decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
