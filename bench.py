@@ -412,27 +412,34 @@ def emit(line: dict) -> None:
 
 
 def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
-    """DRAM bytes of the dominant kernel's launch from the committed `ncu --set
-    full` capture (profiles/r01_ncu_full_gemm_nn_k256_config3.txt: the longest
-    NN launch of the first config-3 pair step, C -= V W2 with the shape in its
-    launch_shape line).  Read from the committed summary, not measured in this run."""
-    prof = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_gemm_nn_k256_config3.txt"
-    if kernel != "gemm_nn" or (m, n) != (69120, 65536) or not prof.is_file():
+    """DRAM bytes of one launch of the dominant kernel from the committed `ncu
+    --set full` captures of the config-3 bench (the longest launch of the first
+    pair step; its shape in the launch_shape line):
+      gemm_nn: profiles/r01_ncu_full_gemm_nn_k256_config3.txt (C -= V W2)
+      gemm_tn: profiles/r01_ncu_full_gemm_tn_k256_config3.txt (W = V^T C)
+    Read from the committed summaries, not measured in this run."""
+    name = {"gemm_nn": "r01_ncu_full_gemm_nn_k256_config3.txt",
+            "gemm_tn": "r01_ncu_full_gemm_tn_k256_config3.txt"}.get(kernel)
+    prof = Path(__file__).resolve().parent / "profiles" / (name or "-")
+    if name is None or (m, n) != (69120, 65536) or not prof.is_file():
         return {}
     vals, shape = {}, None
     for line in prof.read_text().splitlines():
         parts = line.split(",")
         if len(parts) >= 2 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            vals[parts[0]] = float(parts[1]) * 1e9
-        if parts[0] == "launch_shape":
-            shape = tuple(int(x) for x in parts[1:4])
+            unit = parts[2].strip().lower() if len(parts) > 2 else "gbyte"
+            vals[parts[0]] = float(parts[1]) * (1e6 if unit.startswith("m") else 1e9)
+        if parts[0] in ("launch_shape", "launch_shape_tn"):
+            shape = (parts[0], tuple(int(x) for x in parts[1:4]))
     if len(vals) != 2 or shape is None:
         return {}
-    mm, nc, k = shape
-    algo = 8.0 * (2 * mm * nc + mm * k + k * nc)  # C read + write, V, W2
+    kind, (d0, d1, d2) = shape
+    if kind == "launch_shape":        # NN: C (d0 x d1) read + write, V (d0 x d2), W2 (d2 x d1)
+        algo = 8.0 * (2 * d0 * d1 + d0 * d2 + d2 * d1)
+    else:                             # TN: W (d0 x d1) = V^T C, V (d2 x d0), C (d2 x d1)
+        algo = 8.0 * (d2 * d1 + d2 * d0 + d0 * d1)
     return {"traffic": sum(vals.values()), "traffic_unit": "bytes",
-            "traffic_launch": f"one launch {mm}x{nc}x{k} (ncu --set full, "
-                              "profiles/r01_ncu_full_gemm_nn_k256_config3.txt)",
+            "traffic_launch": f"one launch {d0}x{d1}x{d2} (ncu --set full, profiles/{name})",
             "traffic_algorithmic": algo}
 
 

@@ -1226,6 +1226,25 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     int* nf = static_cast<int*>(ws.bar.p) + 8;
     QRB_CUDA_TRY(cudaMemsetAsync(nf, 0, sizeof(int), st));
     static const bool no_switch = std::getenv("QRB_E2E_NO_SWITCH") != nullptr;
+    const int64_t w2 = 2 * int64_t(nb), blk2 = w2 * w2;
+    // Q_k^T for every factored panel k < kc0 on the columns C (left-looking):
+    // pairs with their merged reflector (K = 2nb GEMMs; the TN runs 35.7 instead
+    // of 31.2 TFLOP/s at M = 2nb), single panels otherwise
+    auto apply_prev = [&](int kc0, int64_t c0, int64_t ncols) -> int {
+      for (int k = 0; k < kc0;) {
+        const int64_t j0 = int64_t(k) * nb, mk = h->m - j0;
+        if ((k & 1) == 0 && k + 1 < kc0 && h->t2_valid[k / 2]) {
+          QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), h->T2 + int64_t(k / 2) * blk2, w2,
+                           A.sub(j0, c0, mk, ncols), ws, st));
+          k += 2;
+          continue;
+        }
+        QRB_TRY(apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
+                         A.sub(j0, c0, mk, ncols), ws, st));
+        ++k;
+      }
+      return QRB_OK;
+    };
     for (int64_t c = 0; c < nchunks && status == QRB_OK; ++c) {
       const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
       if (c > 0 && !no_switch && cudaEventQuery(landed[nchunks - 1]) == cudaSuccess) {
@@ -1236,12 +1255,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
         QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[nchunks - 1], 0));
         nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, rem, nf);
         g_launches += 1;
-        const int kc0 = static_cast<int>(col0 / nb);
-        for (int k = 0; k < kc0 && status == QRB_OK; ++k) {
-          const int64_t j0 = int64_t(k) * nb, mk = h->m - j0;
-          status = apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
-                            A.sub(j0, col0, mk, rem), ws, st);
-        }
+        status = apply_prev(static_cast<int>(col0 / nb), col0, rem);
         if (status == QRB_OK) status = right_looking(h, col0, ws, st);
         break;
       }
@@ -1249,17 +1263,24 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
       nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, nc, nf);
       g_launches += 1;
       // left-looking: every earlier panel applied to this chunk, in order
-      const int kc0 = static_cast<int>(col0 / nb);
-      for (int k = 0; k < kc0 && status == QRB_OK; ++k) {
-        const int64_t j0 = int64_t(k) * nb, mk = h->m - j0;
-        status = apply_qt(A.sub(j0, j0, mk, nb), h->T + int64_t(k) * nb * nb, nb,
-                          A.sub(j0, col0, mk, nc), ws, st);
-      }
-      // then the chunk's own panels, right-looking inside the chunk
+      status = apply_prev(static_cast<int>(col0 / nb), col0, nc);
+      // then the chunk's own panels, right-looking inside the chunk (in pairs)
       for (int64_t j0 = col0; j0 < col0 + nc && status == QRB_OK; j0 += nb) {
         const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
         const int k = static_cast<int>(j0 / nb);
         double* Tk = h->T + int64_t(k) * nb * nb;
+        if (g_outer_panels >= 2 && (k & 1) == 0 && j0 + w2 <= col0 + nc && mk >= w2) {
+          double* T2 = nullptr;
+          status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
+                                     h->T2 + int64_t(k / 2) * blk2);
+          if (status != QRB_OK) break;
+          h->t2_valid[k / 2] = 1;
+          const int64_t rest2 = col0 + nc - (j0 + w2);
+          if (rest2 > 0)
+            status = apply_qt(A.sub(j0, j0, mk, w2), T2, w2, A.sub(j0, j0 + w2, mk, rest2), ws, st);
+          j0 += nb;
+          continue;
+        }
         status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
         const int64_t rest = col0 + nc - (j0 + pw);
         if (status == QRB_OK && rest > 0)
