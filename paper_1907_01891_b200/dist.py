@@ -76,6 +76,7 @@ class CudaOps:
     def __init__(self, world: int = 1, side_lookahead: bool = True):
         import torch
         from . import _native
+        self.world = world
         self.lib = _native.load()
         self.native = _native
         # with several ranks a receiver's NCCL kernel can hold SMs while the
@@ -127,6 +128,11 @@ class CudaOps:
         ev.record(main)
         rest = max(nc - first, 0)
         ncap, cap = self._cap_cols(m, w, m_next, nb, rest)
+        if self.world > 1:
+            # keep SMs free for the whole owner step: the broadcast's NCCL kernel is
+            # launched after the side-stream panel and must not wait for a
+            # persistent full-grid update to drain (the other ranks wait for it)
+            ncap = rest
         if ncap:
             self.native.set_tuning("grid_cap", cap)
             try:
