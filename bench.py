@@ -42,6 +42,11 @@ UNIT = "TFLOP/s"
 # 1965 MHz, profiles/r01_fp64_pipe_probe.log (MEASURED_PEAKS.json has no fp64 entry)
 FP64_PEAK_TFLOPS = 37.09
 FP64_PEAK_SOURCE = "measured DMMA peak, profiles/r01_fp64_pipe_probe.log"
+# the other two denominators SURVEY.md 8(d) asks for: nominal B200 FP64 tensor
+# peak, and the measured cuBLAS DGEMM ceiling (torch.matmul fp64 8192^3,
+# profiles/r01_fp64_pipe_probe.log)
+FP64_NOMINAL_TFLOPS = 37.2
+CUBLAS_DGEMM_TFLOPS = 35.47
 CPU_SAMPLE_COLS = 1024
 
 
@@ -381,6 +386,8 @@ def ours_arm(args, rank: int, world: int):
                 "1% Gaussian noise)",
         "config": workload_config(args.config, m, n, S, args.nb),
         "pct_fp64_peak": value / FP64_PEAK_TFLOPS,
+        "pct_fp64_nominal": value / FP64_NOMINAL_TFLOPS,
+        "vs_cublas_dgemm": value / CUBLAS_DGEMM_TFLOPS,
         "slices_per_s": slices_per_s,
         "solve_tflops": solve_flops(m, n, S) / (s_ms * 1e-3) / 1e12,
         "factor_ms": f_ms, "solve_ms": s_ms,

@@ -209,6 +209,48 @@ static int small_product(bool a_kmajor, const MatView& a, const MatView& b, doub
   return QRB_OK;
 }
 
+// Wave-quantisation fix for the long-K TN product W = V^T C (one 128 x 64 tile
+// over all m_k rows per CTA, 4.4 ms at m_k = 69120): the column tiles that fill
+// whole waves of the SMs run as usual, the tail's tiles are split along K into
+// s parts (s minimising ceil(units * s / sms) / s) and reduced in a fixed order.
+// A function of the shape only (deterministic).  Returns false when not worth it.
+static int g_tn_tail = 1;
+static bool tn_tail_split(const MatView& V, const MatView& C, int w, int nc, int m, int64_t ldw,
+                          Workspace& ws, cudaStream_t st) {
+  if (!g_tn_tail) return false;
+  const int G = gemm_sm_count();
+  const int tm = (w + 127) / 128, tn = (nc + 63) / 64;
+  const int units = tm * tn;
+  if (units <= G || units % G == 0 || m < 16 * 256) return false;
+  const int nt1 = (units / G) * G / tm;  // column tiles of the full waves
+  const int rt = tn - nt1, ru = rt * tm;
+  if (nt1 <= 0 || rt <= 0) return false;
+  int best_s = 1;
+  double best = 1.0;  // tail time in units of one full-K tile
+  for (int s = 2; s <= 32 && m / s >= 256; ++s) {
+    const double t = static_cast<double>((ru * s + G - 1) / G) / s;
+    if (t < best - 1e-9) {
+      best = t;
+      best_s = s;
+    }
+  }
+  if (best_s == 1 || best > 0.9) return false;
+  const int64_t n1 = int64_t(nt1) * 64;
+  const int n2 = nc - static_cast<int>(n1);
+  if (gemm_tn(V, C.sub(0, 0, C.rows, n1), ws.W.d(), ldw, 0, w, static_cast<int>(n1), m, 1, 1, 0,
+              st) != QRB_OK)
+    return false;
+  const int64_t per = ldw * n2;
+  int used = 0;
+  if (ws.Wparts.ensure(sizeof(double) * per * best_s, st) != QRB_OK ||
+      gemm_tn_split(V, C.sub(0, n1, C.rows, n2), ws.Wparts.d(), ldw, per, w, n2, m, best_s, 1, 0,
+                    st, &used) != QRB_OK ||
+      reduce_splits(ws.Wparts.d(), per, used, w, n2, ldw, ws.W.d() + n1 * ldw, ldw, st) != QRB_OK)
+    return false;
+  g_launches += 3;
+  return true;
+}
+
 // W2 = T^T (V^T C) into ws.W2 (w x nc, ld even(w)); V m x w unit lower (in place under R)
 static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const MatView& C,
                        Workspace& ws, cudaStream_t st) {
@@ -231,7 +273,7 @@ static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const Mat
                             &used));
       QRB_TRY(reduce_splits(ws.Wparts.d(), per_split, used, w, nc, ldw, ws.W.d(), ldw, st));
       g_launches += 2;
-    } else {
+    } else if (!tn_tail_split(V, C, w, nc, m, ldw, ws, st)) {
       QRB_TRY(gemm_tn(V, C, ws.W.d(), ldw, 0, w, nc, m, 1, 1, 0, st));
       g_launches += 1;
     }
@@ -1686,6 +1728,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     gemm_set_nn_dynamic(value == 1);
     return QRB_OK;
   }
+  if (k == "tn_tail" && (value == 0 || value == 1)) {
+    g_tn_tail = static_cast<int>(value);
+    return QRB_OK;
+  }
   if (k == "grid_cap" && value >= 0) {  // this host thread's GEMM grid cap (0 = none)
     gemm_set_grid_cap(static_cast<int>(value));
     return QRB_OK;
@@ -1722,6 +1768,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "outer_panels") *value = g_outer_panels;
   else if (k == "lookahead") *value = g_lookahead;
   else if (k == "grid_cap") *value = gemm_grid_cap();
+  else if (k == "tn_tail") *value = g_tn_tail;
   else if (k == "sm_count") *value = gemm_sm_count();
   else if (k == "la_sms") *value = g_la_sms;
   else if (k == "la_lat_us") *value = g_la_lat_us;

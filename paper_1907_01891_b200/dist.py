@@ -463,8 +463,8 @@ def bench_rank(args, rank: int, world: int):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", local_rank))
-    from bench import (FP64_PEAK_TFLOPS, METRIC, UNIT, ClockSampler, build_workload, emit,
-                       qr_flops, solve_flops)
+    from bench import (CUBLAS_DGEMM_TFLOPS, FP64_NOMINAL_TFLOPS, FP64_PEAK_TFLOPS, METRIC, UNIT,
+                       ClockSampler, build_workload, emit, qr_flops, solve_flops)
     from . import ct_system as cs
     from .device import QrDevice, launch_count
 
@@ -623,6 +623,8 @@ def bench_rank(args, rank: int, world: int):
                                       f"over {world} GPUs, NCCL block broadcast, owner "
                                       f"look-ahead on a side stream; slices split for the solve"},
             "pct_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
+            "pct_fp64_nominal": value / (FP64_NOMINAL_TFLOPS * world),
+            "vs_cublas_dgemm": value / (CUBLAS_DGEMM_TFLOPS * world),
             "slices_per_s": S / float(s_s),
             "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,
             "factor_ms": float(f_s) * 1e3, "gather_ms": float(np.mean(gs)) * 1e3,

@@ -79,3 +79,46 @@ def test_config3_size_independent_properties():
     q.solve_device(b, x2, torch.zeros_like(r))
     assert torch.equal(x1, x2)
     q.close()
+
+
+def test_config2_against_reference_golden():
+    """BASELINE config 2 against the REFERENCE package itself
+    (tests/golden/make_golden_cfg2.py: oocqr factorize + solve on the same
+    Siddon matrix, tile 2048, inner block 128): X <= 1e-8, residual <= 1e-9,
+    |diag R| and the first rows of R (row signs normalised) <= 1e-10."""
+    import hashlib
+    from pathlib import Path
+
+    import torch
+    from paper_1907_01891_b200.device import QrDevice
+    fx = Path(__file__).resolve().parent / "golden" / "ref_ct2.npz"
+    if not fx.is_file():
+        pytest.skip("config-2 reference fixture not generated")
+    ref = np.load(fx)
+    g = cs.config_geometry(2)
+    m, n = g.n_rays, g.n_pixels
+    assert str(ref["geometry_hash"]) == cs.geometry_hash(g)
+    lda = (m + 31) // 32 * 32
+    a = cs.densify_device(g, lda)
+    a_host = np.ascontiguousarray(a[:, :m].cpu().numpy().T)          # same bytes, C order
+    assert hashlib.sha256(a_host.tobytes()).hexdigest() == str(ref["a_sha256"])
+    del a_host
+    bm = ref["b"]
+    b = torch.zeros((bm.shape[1], lda), dtype=torch.float64, device="cuda")
+    b[:, :m] = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda()
+    q = QrDevice(m, n)
+    q.set_matrix_device(a)
+    q.factorize()
+    x = torch.zeros((bm.shape[1], n), dtype=torch.float64, device="cuda")
+    r = torch.zeros(bm.shape[1], dtype=torch.float64, device="cuda")
+    q.solve_device(b, x, r)
+    xr = ref["x"]
+    assert np.abs(x.cpu().numpy().T - xr).max() <= 1e-8 * np.abs(xr).max()
+    np.testing.assert_allclose(r.cpu().numpy(), ref["resid"], rtol=1e-9)
+    rd = np.abs(q.rdiag())
+    assert np.abs(rd - ref["rdiag_abs"]).max() <= 1e-10 * ref["rdiag_abs"].max()
+    rows = q.get_matrix(0, n)[:4]                                     # 4 x n
+    rows = np.array([np.where(np.arange(n) >= i, rows[i], 0.0) for i in range(4)])
+    rows = rows * np.sign(np.diag(rows[:, :4]))[:, None]
+    assert np.abs(rows - ref["r_rows4"]).max() <= 1e-10 * np.abs(ref["r_rows4"]).max()
+    q.close()
