@@ -132,3 +132,23 @@ def test_oracle_matches_reference_ct(golden, cfg):
         assert rel_err(sign_normalise(f.r()), ref["r_signed"]) <= 1e-12
     else:
         assert rel_err(sign_normalise(f.r())[:32], ref["r_rows32"]) <= 1e-12
+
+
+def test_config2_reference_fixture_inputs():
+    """tests/golden/ref_ct2.npz (the reference package's factorize + solve of
+    BASELINE config 2, make_golden_cfg2.py) was made from exactly the matrix
+    and sinograms this repository generates: pinned by sha256."""
+    import hashlib
+    from pathlib import Path
+
+    from paper_1907_01891_b200 import ct_system as cs
+    ref = np.load(Path(__file__).resolve().parent / "golden" / "ref_ct2.npz")
+    g = cs.config_geometry(2)
+    assert str(ref["geometry_hash"]) == cs.geometry_hash(g)
+    a = cs.dense_matrix(g, order="C")
+    assert hashlib.sha256(a.tobytes()).hexdigest() == str(ref["a_sha256"])
+    x_true = cs.phantom_stack(2, ref["b"].shape[1])
+    b = cs.noisy_sinograms(a @ x_true, 2)
+    assert np.array_equal(b, ref["b"])
+    # the reference's residuals are those of its own solution
+    assert np.allclose(np.linalg.norm(a @ ref["x"] - b, axis=0), ref["resid"], rtol=1e-12)
