@@ -148,6 +148,44 @@ def densify_device(g, coo, lda: int):
     return a
 
 
+def measure_config(cfg: int, reps: int = 3) -> dict:
+    """QR TFLOP/s and slices/s of another BASELINE configuration on this GPU
+    (device-resident A and B, best of `reps` after a warm-up; reported beside
+    the headline, not part of it)."""
+    import torch
+    from paper_1907_01891_b200 import ct_system as cs
+    from paper_1907_01891_b200.device import QrDevice
+    g = cs.config_geometry(cfg)
+    m, n = g.n_rays, g.n_pixels
+    S = cs.CONFIGS[cfg]["slices"]
+    lda = (m + 31) // 32 * 32
+    a = cs.densify_device(g, lda)
+    xt = torch.from_numpy(np.ascontiguousarray(cs.phantom_stack(cfg, S).T)).cuda()   # (S, n)
+    bh = cs.noisy_sinograms((xt @ a[:, :m]).cpu().numpy().T, cfg)                   # (m, S)
+    b = torch.zeros((S, lda), dtype=torch.float64, device="cuda")
+    b[:, :m] = torch.from_numpy(np.ascontiguousarray(bh.T)).cuda()
+    x = torch.zeros((S, n + (n & 1)), dtype=torch.float64, device="cuda")
+    q = QrDevice(m, n)
+    fms, sms = [], []
+    for it in range(reps + 1):
+        q.set_matrix_device(a)
+        f = q.factorize()["total_ms"]
+        s_ = q.solve_device(b, x)["total_ms"]
+        if it:
+            fms.append(f)
+            sms.append(s_)
+    q.close()
+    f_ms, s_ms = min(fms), min(sms)
+    out = {"workload": f"config{cfg}: QR of A {m}x{n} + solve {S} slices", "m": m, "n": n,
+           "slices": S, "qr_tflops": qr_flops(m, n) / (f_ms * 1e-3) / 1e12,
+           "pct_fp64_peak": qr_flops(m, n) / (f_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+           "factor_ms": f_ms, "solve_ms": s_ms, "slices_per_s": S / (s_ms * 1e-3),
+           "timing": f"best of {reps} after a warm-up, device-resident A and B"}
+    del a, b, x, xt
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_sample_tflops(coo, g, steps: int = 1, a_sample=None):
     """Reference algorithm (oracle port, tiled left-looking QR of oocqr) on the
     leading m x 1024 column block of A; returns (TFLOP/s, seconds per run)."""
@@ -375,6 +413,11 @@ def ours_arm(args, rank: int, world: int):
            "path": "QrDevice.factorize_host(pinned host A; chunked H2D overlapped with the "
                    "left-looking chunk order) + solve(host B -> host X)"}
     q.close()
+    del a_pin, b_pin, x_pin
+    others = {}
+    if args.config == 3 and args.other_configs:
+        for c in (1, 2):
+            others[f"config{c}"] = measure_config(c)
 
     cores = len(os.sched_getaffinity(0))
     cpu_val, cpu_t, ncol = cpu_sample_tflops(None, g, a_sample=a_sample)
@@ -396,7 +439,7 @@ def ours_arm(args, rank: int, world: int):
                          "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
                                    f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
-        "config5": cfg5, "quality": quality,
+        "config5": cfg5, "other_configs": others or None, "quality": quality,
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s, "densify_s": densify_s,
     }
@@ -462,6 +505,8 @@ def main():
     ap.add_argument("--cfg5-slices", type=int, default=4096,
                     help="slices of the config-5 solve-throughput run (0 = skip)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--other-configs", type=int, default=1,
+                    help="with config 3: also report configs 1 and 2 on this GPU (1) or not (0)")
     ap.add_argument("--lean-solve", action="store_true",
                     help="multi-GPU: stream V and R instead of replicating the factors")
     ap.add_argument("--force-dist", action="store_true",
