@@ -244,9 +244,11 @@ QRB_API int qrb_release_workspace(void);
  * reference's only backend switch is kernels.use_path, kernels.py:265-283).
  *   "panel_algo"       0 auto | 1 Householder columns | 2 CholeskyQR2 when the shape allows
  *   "cholqr_min_rows"  auto mode uses CholeskyQR2 for panels with at least this many rows
- *   "outer_panels"     2 (default): panels are factored in pairs and the trailing update
- *                      uses the merged 2nb-wide block reflector (K = 2nb GEMMs); 1: one by one;
- *                      4: two pairs merged (K = 4nb; qrb_factorize / qrb_factorize_host only)
+ *   "outer_panels"     4 (default): while "outer4_min_cols" (24576) trailing columns remain,
+ *                      two panel pairs are merged into one 4nb-wide block reflector
+ *                      (K = 4nb trailing-update GEMMs), then pairs (K = 2nb); 2: pairs only;
+ *                      1: one panel at a time (qrb_factorize / qrb_factorize_host)
+ *   "tn_tail"          1 (default): the W = V^T C product's last partial wave split along K
  *   "nn_dynamic"       1: the persistent trailing-update GEMM hands out tiles dynamically
  *                      (for multi-GPU runs, where NCCL kernels may hold SMs); 0: static
  *   "lookahead"        1 (default): while the trailing update of panel pair s runs on

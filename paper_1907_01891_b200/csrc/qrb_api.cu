@@ -496,7 +496,7 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
 // Panels per outer step (qrb_set_tuning "outer_panels": 1 or 2).
 static int g_outer_panels = [] {
   const char* e = std::getenv("QRB_OUTER_PANELS");
-  if (!e) return 2;
+  if (!e) return 4;
   const int v = std::atoi(e);
   return v >= 4 ? 4 : std::max(1, std::min(2, v));
 }();
@@ -858,6 +858,11 @@ static int g_la_sms = 24;              // SMs left to the look-ahead panel (r01 
 static int64_t g_la_lat_us = 250;      // latency part of a pair's panel chain (r01 sweep)
 static int64_t g_la_margin_pct = 25;   // capped window = (1 + margin) x modelled panel time
 static std::atomic<int64_t> g_la_steps{0};
+// outer_panels = 4 (default): 4-panel blocks while >= 24576 trailing columns
+// remain, pairs after (r01 sweep at config 3: pairs only 34.49, 4-panel blocks
+// to 16384 / 32768 / 49152 remaining columns 34.75 / 34.75 / 34.63 TFLOP/s;
+// config 2 (16384 columns) never takes them)
+static int64_t g_outer4_min_cols = 24576;
 
 static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_t st) {
   const int nb = h->nb;
@@ -867,6 +872,10 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   const int64_t wq = q * int64_t(nb), blkq = wq * wq;
   MatView A{h->A, m, n, h->lda};
   auto block_here = [&](int64_t j0, int64_t w) {
+    // 4-panel blocks only while at least g_outer4_min_cols trailing columns
+    // remain (their K = 4nb update pays where the update is long; late steps
+    // take pairs, whose shorter panel chain hides better)
+    if (w > w2 && n - j0 - w < g_outer4_min_cols) return false;
     return g_outer_panels >= 2 && j0 + w < n && m - j0 >= w;
   };
   // merged reflector storage: pairs starting at an even panel are kept for the
@@ -1728,6 +1737,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     gemm_set_nn_dynamic(value == 1);
     return QRB_OK;
   }
+  if (k == "outer4_min_cols" && value >= 0) {
+    g_outer4_min_cols = value;
+    return QRB_OK;
+  }
   if (k == "tn_tail" && (value == 0 || value == 1)) {
     g_tn_tail = static_cast<int>(value);
     return QRB_OK;
@@ -1769,6 +1782,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "lookahead") *value = g_lookahead;
   else if (k == "grid_cap") *value = gemm_grid_cap();
   else if (k == "tn_tail") *value = g_tn_tail;
+  else if (k == "outer4_min_cols") *value = g_outer4_min_cols;
   else if (k == "sm_count") *value = gemm_sm_count();
   else if (k == "la_sms") *value = g_la_sms;
   else if (k == "la_lat_us") *value = g_la_lat_us;

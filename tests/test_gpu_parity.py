@@ -222,22 +222,27 @@ def test_kernels_actually_launch():
     assert launch_count() > before + 10
 
 
-@pytest.mark.parametrize("m,n", [(2160, 1024), (3001, 1537)])
-def test_lookahead_factorization_matches_oracle_and_is_deterministic(m, n):
+@pytest.mark.parametrize("m,n,outer", [(2160, 1024, 2), (3001, 1537, 2), (2160, 1024, 4),
+                                       (3001, 1537, 4)])
+def test_lookahead_factorization_matches_oracle_and_is_deterministic(m, n, outer):
     """Single-GPU look-ahead (qrb_api.cu right_looking): the next panel pair is
     factored on a side stream while the trailing update runs on capped GEMM
     grids.  Forced on at test sizes (lookahead = 2), checked against the serial
     schedule (bitwise), the oracle's R up to row signs and for run-to-run
-    determinism."""
+    determinism.  outer = 4: 4-panel blocks (two merged pairs, K = 4nb updates)
+    forced at this size (outer4_min_cols = 0)."""
     import torch
     from paper_1907_01891_b200 import _native
     from paper_1907_01891_b200.device import QrDevice
     rng = np.random.default_rng(m)
     A = rng.standard_normal((m, n))
     B = A @ rng.standard_normal((n, 3)) + 1e-3 * rng.standard_normal((m, 3))
-    keys = {k: _native.get_tuning(k) for k in ("lookahead", "la_lat_us", "la_sms")}
+    keys = {k: _native.get_tuning(k) for k in ("lookahead", "la_lat_us", "la_sms", "outer_panels",
+                                                 "outer4_min_cols")}
     try:
         _native.set_tuning("la_sms", 32)
+        _native.set_tuning("outer_panels", outer)
+        _native.set_tuning("outer4_min_cols", 0)
         out = {}
         for la in (0, 2, 2):
             _native.set_tuning("lookahead", la)

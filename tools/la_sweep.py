@@ -13,7 +13,8 @@ m, n = g.n_rays, g.n_pixels
 a = cs.densify_device(g, (m + 31) // 32 * 32)
 fl = 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
 q = QrDevice(m, n)
-defaults = {k: _native.get_tuning(k) for k in ("lookahead", "la_sms", "la_lat_us", "la_margin_pct")}
+defaults = {k: _native.get_tuning(k) for k in ("lookahead", "la_sms", "la_lat_us", "la_margin_pct",
+                                               "outer_panels", "outer4_min_cols", "tn_tail")}
 for spec in sys.argv[2:]:
     for k, v in defaults.items():
         _native.set_tuning(k, v)
