@@ -465,11 +465,13 @@ def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
     """DRAM bytes of one launch of the dominant kernel from the committed `ncu
     --set full` captures of the config-3 bench (the longest launch of the first
     pair step; its shape in the launch_shape line):
-      gemm_nn: profiles/r01_ncu_full_gemm_nn_k256_config3.txt (C -= V W2)
-      gemm_tn: profiles/r01_ncu_full_gemm_tn_k256_config3.txt (W = V^T C)
+      gemm_nn: profiles/r01_ncu_full_gemm_nn_k512_config3.txt (C -= V W2)
+      gemm_tn: profiles/r01_ncu_full_gemm_tn_k512_config3.txt (W = V^T C)
+    (the first steps use 4-panel blocks; K = 256 captures of the pair steps are
+    kept beside them as *_k256_*).
     Read from the committed summaries, not measured in this run."""
-    name = {"gemm_nn": "r01_ncu_full_gemm_nn_k256_config3.txt",
-            "gemm_tn": "r01_ncu_full_gemm_tn_k256_config3.txt"}.get(kernel)
+    name = {"gemm_nn": "r01_ncu_full_gemm_nn_k512_config3.txt",
+            "gemm_tn": "r01_ncu_full_gemm_tn_k512_config3.txt"}.get(kernel)
     prof = Path(__file__).resolve().parent / "profiles" / (name or "-")
     if name is None or (m, n) != (69120, 65536) or not prof.is_file():
         return {}

@@ -24,6 +24,21 @@ int modified_lu_blk(const double* Qt, int ldq, int b, double* Uc, double* NUcS, 
                     double* Ucinv, double* L1invT, double* s, int ldo, int* flag, int bit,
                     cudaStream_t stream);
 
+// C_p = A_p B_p for up to kMax independent products with M, N, K <= 128
+// (column-major, any leading dimensions), one launch
+struct SmallMm {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int M, N, K;
+};
+struct SmallMmBatch {
+  static constexpr int kMax = 4;
+  SmallMm p[kMax];
+};
+int small_mm_batch(const SmallMmBatch& batch, int count, cudaStream_t stream);
+
 // P[0:b,0:b] <- diag(s) R on/above the diagonal, L1 below; tau_k = T_kk.
 int cholqr_write_top(double* P, int64_t ldp, int b, const double* R, const double* s,
                      const double* L1, const double* T, int64_t ldt, double* tau, int ldo,

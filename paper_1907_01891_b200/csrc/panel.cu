@@ -341,24 +341,37 @@ __global__ void __launch_bounds__(BT_THREADS) build_t_kernel(const double* G, in
 }
 
 // W = sum_s parts[s]   (fixed order, deterministic)
+// out = sum over z of parts_z.  TPE threads per element (consecutive lanes)
+// each sum every TPE-th split in two chains, then combine by xor shuffles: a
+// fixed order, so the result is deterministic; more loads in flight than one
+// thread per element (the Gram partials are read right after they are written,
+// from L2: latency-bound with few elements and many splits)
+template <int TPE>
 __global__ void reduce_splits_kernel(const double* parts, int64_t split_stride, int splits,
                                      int rows, int cols, int64_t ldp, double* out, int64_t ldo) {
   const int64_t total = (int64_t)rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = idx / rows, r = idx - c * rows;
-    const double* src = parts + r + c * ldp;
-    // 4 independent partial chains (loads in flight), combined in fixed order
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int z = 0;
-    for (; z + 4 <= splits; z += 4) {
-      s0 += src[(int64_t)(z + 0) * split_stride];
-      s1 += src[(int64_t)(z + 1) * split_stride];
-      s2 += src[(int64_t)(z + 2) * split_stride];
-      s3 += src[(int64_t)(z + 3) * split_stride];
+  const int sub = threadIdx.x % TPE, lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / TPE;;
+       base += (int64_t)gridDim.x * blockDim.x / TPE) {
+    if (base - lane / TPE >= total) break;  // warp-uniform: the shuffles need every lane
+    const bool valid = base < total;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t r = 0, c = 0;
+    if (valid) {
+      c = base / rows;
+      r = base - c * rows;
+      const double* src = parts + r + c * ldp;
+      int z = sub;
+      for (; z + TPE < splits; z += 2 * TPE) {
+        s0 += src[(int64_t)z * split_stride];
+        s1 += src[(int64_t)(z + TPE) * split_stride];
+      }
+      if (z < splits) s0 += src[(int64_t)z * split_stride];
     }
-    for (; z < splits; ++z) s0 += src[(int64_t)z * split_stride];
-    out[r + c * ldo] = (s0 + s1) + (s2 + s3);
+    double v = s0 + s1;
+#pragma unroll
+    for (int o = 1; o < TPE; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (valid && sub == 0) out[r + c * ldo] = v;
   }
 }
 
@@ -612,9 +625,27 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
                   int64_t ldp, double* out, int64_t ldo, cudaStream_t stream) {
   const int64_t total = (int64_t)rows * cols;
   if (total == 0) return QRB_OK;
-  int blocks = static_cast<int>(std::min<int64_t>((total + 127) / 128, 8 * 148));
-  reduce_splits_kernel<<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols, ldp,
-                                                   out, ldo);
+  const int tpe = splits <= 8 ? 1 : splits <= 16 ? 2 : splits <= 32 ? 4 : 8;
+  // whole warps per grid-stride round, so the shuffles see full groups
+  const int64_t threads = ((total * tpe + 127) / 128) * 128;
+  const int blocks = static_cast<int>(std::min<int64_t>(threads / 128, 16 * 148));
+  switch (tpe) {
+    case 1:
+      reduce_splits_kernel<1><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
+                                                          ldp, out, ldo);
+      break;
+    case 2:
+      reduce_splits_kernel<2><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
+                                                          ldp, out, ldo);
+      break;
+    case 4:
+      reduce_splits_kernel<4><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
+                                                          ldp, out, ldo);
+      break;
+    default:
+      reduce_splits_kernel<8><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
+                                                          ldp, out, ldo);
+  }
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
 }

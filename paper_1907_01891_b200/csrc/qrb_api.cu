@@ -388,17 +388,22 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
   // pass 2: G2 = Q1^T Q1 (must be close to I), R2 = chol(G2)
   QRB_TRY(gram(Q1));
   QRB_TRY(chol_inv(ws.G.d(), LD, b, R2, R2i, LD, flag, 2, 1, st));
-  // top block of Q = Q1 R2^-1, modified LU, small products
-  QRB_TRY(gemm_nn(MatView{Wq, b, b, mw}, MatView{R2i, b, b, LD}, Qt, LD, b, b, b, GEMM_EPI_STORE,
-                  0, st));
+  // top block of Q = Q1 R2^-1 and R = R2 R1 (one batched launch), modified LU,
+  // then M = R2^-1 Uc^-1 and T^T = -Uc S L1^-T (one batched launch)
+  {
+    SmallMmBatch bt{};
+    bt.p[0] = SmallMm{Wq, R2i, Qt, mw, LD, LD, b, b, b};
+    bt.p[1] = SmallMm{R2, R1, R, LD, LD, LD, b, b, b};
+    QRB_TRY(small_mm_batch(bt, 2, st));
+  }
   QRB_TRY(modified_lu(Qt, LD, b, Uc, NUcS, L1, Uci, L1iT, s, LD, flag, 4, st));
-  QRB_TRY(gemm_nn(MatView{R2i, b, b, LD}, MatView{Uci, b, b, LD}, M, LD, b, b, b, GEMM_EPI_STORE,
-                  0, st));
-  QRB_TRY(gemm_nn(MatView{R2, b, b, LD}, MatView{R1, b, b, LD}, R, LD, b, b, b, GEMM_EPI_STORE, 0,
-                  st));
-  QRB_TRY(gemm_nn(MatView{NUcS, b, b, LD}, MatView{L1iT, b, b, LD}, Tt, LD, b, b, b,
-                  GEMM_EPI_STORE, 0, st));
-  g_launches += 10;
+  {
+    SmallMmBatch bt{};
+    bt.p[0] = SmallMm{R2i, Uci, M, LD, LD, LD, b, b, b};
+    bt.p[1] = SmallMm{NUcS, L1iT, Tt, LD, LD, LD, b, b, b};
+    QRB_TRY(small_mm_batch(bt, 2, st));
+  }
+  g_launches += 8;
   QRB_CUDA_TRY(cudaMemcpyAsync(ws.hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   QRB_CUDA_TRY(cudaStreamSynchronize(st));
   ++g_cholqr_panels;
