@@ -511,6 +511,8 @@ def main():
                     help="with config 3: also report configs 1 and 2 on this GPU (1) or not (0)")
     ap.add_argument("--lean-solve", action="store_true",
                     help="multi-GPU: stream V and R instead of replicating the factors")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: functional check of the multi-rank path with ranks sharing one GPU")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()

@@ -458,11 +458,20 @@ def bench_rank(args, rank: int, world: int):
     import torch.distributed as dist
 
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    backend = getattr(args, "dist_backend", "nccl")
+    if backend == "gloo":
+        # functional check of this multi-rank bench path on a one-GPU box: the
+        # ranks share the GPU and exchange through host memory (no performance
+        # meaning; the driver's multi-GPU runs use NCCL, one GPU per rank)
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", local_rank))
+    if backend == "gloo":
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local_rank))
     from bench import (CUBLAS_DGEMM_TFLOPS, FP64_NOMINAL_TFLOPS, FP64_PEAK_TFLOPS, METRIC, UNIT,
                        ClockSampler, build_workload, emit, qr_flops, solve_flops)
     from . import ct_system as cs

@@ -54,3 +54,30 @@ def test_single_rank_nccl_factor_gather_solve():
         np.testing.assert_allclose(r2.cpu().numpy(), orc.residual_norms(ref, bm), rtol=1e-9)
     finally:
         dist.destroy_process_group()
+
+
+def test_bench_multirank_path_two_ranks_gloo(tmp_path):
+    """bench.py's multi-GPU path (dist.bench_rank: per-rank Siddon densify,
+    all-reduced sinograms, block-cyclic factorization with the owner's side-
+    stream look-ahead, gather, slice-split solve, e2e) end to end with 2 ranks
+    under torchrun -- here over gloo with both ranks on the one GPU, so the
+    control flow of an N = 2 run is exercised (not its performance)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
+           "--gpus", "2", "--config", "2", "--dist-backend", "gloo", "--steps", "1",
+           "--warmup", "1"]
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["slices_per_s"] > 0 and line["gpu_launches"] > 0
