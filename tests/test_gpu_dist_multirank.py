@@ -25,7 +25,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, m, n, nb, out_dir, lookahead, bw, side):
+def _worker(rank, world, port, m, n, nb, out_dir, lookahead, bw, side, h2d=False):
     import torch.distributed as dist
 
     from paper_1907_01891_b200 import dist as qd
@@ -41,8 +41,12 @@ def _worker(rank, world, port, m, n, nb, out_dir, lookahead, bw, side):
         full[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
         a_local = qd.scatter_block_cyclic(full, n, bw, rank, world)
         ops = qd.CudaOps(world, side_lookahead=side)
+        host = None
+        if h2d:  # local blocks streamed in from pinned host memory during the first steps
+            host = a_local.cpu().pin_memory()
+            a_local.zero_()
         f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, ops,
-                                     lookahead=lookahead, bw=bw)
+                                     lookahead=lookahead, bw=bw, host_src=host, chunk_cols=192)
         fact = qd.gather_factored(f)
         bmat = rng.standard_normal((m, 6))
         first, cnt = qd.slice_share(6, rank, world)
@@ -66,17 +70,21 @@ def _worker(rank, world, port, m, n, nb, out_dir, lookahead, bw, side):
                                                      (2, 1500, 700, 64, True, 128, True),
                                                      (3, 1100, 900, 64, True, 128, True),
                                                      (1, 1500, 1000, 64, True, 128, True),
-                                                     (2, 900, 500, 32, False, 64, True)])
+                                                     (2, 900, 500, 32, False, 64, True),
+                                                     (2, 1500, 1000, 64, True, 128, "h2d"),
+                                                     (1, 1500, 1000, 64, True, 128, "h2d")])
 def test_multirank_cuda_schedule_matches_oracle(tmp_path, world, m, n, nb, la, bw, side):
     """bw = 2 nb: panel-pair blocks (qrb_op_panel_block); side: the owner's next
-    block factored + broadcast on a side stream under its capped update."""
+    block factored + broadcast on a side stream under its capped update; "h2d":
+    the local blocks copied in from pinned host memory by chunks during the
+    first steps (host_src)."""
     import torch.multiprocessing as mp
 
     from conftest import rel_err, sign_normalise
     from oracle import tiled_qr as orc
 
-    mp.spawn(_worker, args=(world, _free_port(), m, n, nb, str(tmp_path), la, bw, side),
-             nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), m, n, nb, str(tmp_path), la, bw, bool(side),
+                            side == "h2d"), nprocs=world, join=True)
     a = np.load(tmp_path / "a.npy")
     bmat = np.load(tmp_path / "b.npy")
     fact = np.load(tmp_path / "factored.npy")
