@@ -91,6 +91,10 @@ CONFIGS = {
     3: dict(image=256, views=180, bins=384, slices=256),
     4: dict(image=512, views=720, bins=375, slices=64),
     5: dict(image=256, views=180, bins=384, slices=4096),
+    # config 4's geometry family at 1/8 the image width (views/W and bins/W kept:
+    # 720/512 -> 90/64, 375/512 -> 47/64; m/n = 1.03 as at full size): the
+    # reduced instance the reference can factor here
+    6: dict(image=64, views=90, bins=47, slices=8),
 }
 
 

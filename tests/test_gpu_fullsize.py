@@ -122,3 +122,37 @@ def test_config2_against_reference_golden():
     rows = rows * np.sign(np.diag(rows[:, :4]))[:, None]
     assert np.abs(rows - ref["r_rows4"]).max() <= 1e-10 * np.abs(ref["r_rows4"]).max()
     q.close()
+
+
+def test_reduced_config4_family_against_reference_golden():
+    """Config 4's geometry family at 1/8 width (4230 x 4096, m/n = 1.03): the
+    GPU factorization + solve against the reference package's own result
+    (tests/golden/make_golden_cfg4r.py) -- the parity pin for config 4, whose
+    566 GB the reference cannot factor here."""
+    from pathlib import Path
+
+    import torch
+    from paper_1907_01891_b200.device import QrDevice
+    ref = np.load(Path(__file__).resolve().parent / "golden" / "ref_ct4r.npz")
+    g = cs.config_geometry(6)
+    m, n = g.n_rays, g.n_pixels
+    lda = (m + 31) // 32 * 32
+    a = cs.densify_device(g, lda)
+    bm = ref["b"]
+    b = torch.zeros((bm.shape[1], lda), dtype=torch.float64, device="cuda")
+    b[:, :m] = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda()
+    q = QrDevice(m, n)
+    q.set_matrix_device(a)
+    q.factorize()
+    x = torch.zeros((bm.shape[1], n), dtype=torch.float64, device="cuda")
+    r = torch.zeros(bm.shape[1], dtype=torch.float64, device="cuda")
+    q.solve_device(b, x, r)
+    xr = ref["x"]
+    assert np.abs(x.cpu().numpy().T - xr).max() <= 1e-8 * np.abs(xr).max()
+    np.testing.assert_allclose(r.cpu().numpy(), ref["resid"], rtol=1e-9)
+    assert np.abs(np.abs(q.rdiag()) - ref["rdiag_abs"]).max() <= 1e-10 * ref["rdiag_abs"].max()
+    rows = q.get_matrix(0, n)[:8]
+    rows = np.array([np.where(np.arange(n) >= i, rows[i], 0.0) for i in range(8)])
+    rows = rows * np.sign(np.diag(rows[:, :8]))[:, None]
+    assert np.abs(rows - ref["r_rows8"]).max() <= 1e-10 * np.abs(ref["r_rows8"]).max()
+    q.close()

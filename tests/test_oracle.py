@@ -152,3 +152,28 @@ def test_config2_reference_fixture_inputs():
     assert np.array_equal(b, ref["b"])
     # the reference's residuals are those of its own solution
     assert np.allclose(np.linalg.norm(a @ ref["x"] - b, axis=0), ref["resid"], rtol=1e-12)
+
+
+def test_oracle_matches_reference_on_reduced_config4_family():
+    """Config 4's geometry family at 1/8 width (ct_system CONFIGS[6], 4230 x 4096,
+    m/n = 1.03 as at full size): the oracle's tiled factorization and solve
+    equal the reference package's (tests/golden/make_golden_cfg4r.py) on the
+    same bytes."""
+    import hashlib
+    from pathlib import Path
+
+    from paper_1907_01891_b200 import ct_system as cs
+    ref = np.load(Path(__file__).resolve().parent / "golden" / "ref_ct4r.npz")
+    g = cs.config_geometry(6)
+    assert str(ref["geometry_hash"]) == cs.geometry_hash(g)
+    a = cs.dense_matrix(g, order="C")
+    assert hashlib.sha256(a.tobytes()).hexdigest() == str(ref["a_sha256"])
+    b = cs.noisy_sinograms(a @ cs.phantom_stack(6, ref["b"].shape[1]), 6)
+    assert np.array_equal(b, ref["b"])
+    f = orc.factorize_dense(a, 512, 128)
+    x = orc.solve_dense(f, b)
+    assert np.abs(x - ref["x"]).max() <= 1e-12 * np.abs(ref["x"]).max()
+    r = f.r()
+    s = np.sign(np.diag(r))
+    s[s == 0] = 1.0
+    assert np.abs((r * s[:, None])[:8] - ref["r_rows8"]).max() <= 1e-12 * np.abs(ref["r_rows8"]).max()
