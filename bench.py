@@ -412,6 +412,14 @@ def ours_arm(args, rank: int, world: int):
            "h2d_ms_overlapped": frep_e2e["h2d_ms"],
            "path": "QrDevice.factorize_host(pinned host A; chunked H2D overlapped with the "
                    "left-looking chunk order) + solve(host B -> host X)"}
+    # the host-API result against the device-path result of the timed steps (the
+    # two factorizations run the columns in a different order: rounding only)
+    xd = x_dev[:, :n].cpu().numpy().T
+    rd = r_dev.cpu().numpy()
+    e2e["check"] = {"x_max_rel_vs_device_path": float(np.abs(x_view - xd).max() / np.abs(xd).max()),
+                    "resid_max_rel_vs_device_path":
+                        float((np.abs(np.asarray(resid_host) - rd) / np.abs(rd)).max())}
+    del xd, rd
     q.close()
     del a_pin, b_pin, x_pin
     others = {}
