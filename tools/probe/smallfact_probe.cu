@@ -1,9 +1,10 @@
 // Standalone correctness / timing probe of the blocked small factorizations
 // (csrc/smallfact.cu) against their definitions and against the sweep kernels
-// (csrc/cholqr.cu).  Build + run on the GPU box:
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/sfp \
-//     tools/probe/smallfact_probe.cu paper_1907_01891_b200/csrc/cholqr.cu \
-//     paper_1907_01891_b200/csrc/smallfact.cu && /tmp/sfp
+// (csrc/cholqr.cu).  Build (here; -DSF_TRACE adds per-phase cycle counts) and
+// run on the GPU box:
+//   nvcc -DSF_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//     -o tools/probe/smallfact_probe tools/probe/smallfact_probe.cu \
+//     paper_1907_01891_b200/csrc/cholqr.cu paper_1907_01891_b200/csrc/smallfact.cu
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -25,7 +26,9 @@ int set_max_dynamic_smem(const void* f, size_t bytes) {  // once per kernel, lik
              ? 0
              : -1;
 }
+#ifdef SF_TRACE
 void smallfact_trace(long long* out);
+#endif
 }  // namespace qrb
 
 static const int LD = 128;
@@ -196,6 +199,7 @@ int main() {
            b, e3, e4, e5, e6, (int)sgn, hf, ok2 ? "OK" : "FAIL", tb2, tl2);
     cudaFree(flag);
   }
+#ifdef SF_TRACE
   long long tr[3][32];
   qrb::smallfact_trace(&tr[0][0]);
   const char* names[3] = {"chol", "mlu", "triinv"};
@@ -205,6 +209,7 @@ int main() {
     printf("\n");
   }
   printf("chol load %lld  output %lld\n", tr[0][0] - tr[0][31], tr[0][29] - tr[0][30]);
+#endif
   printf("%s (%s)\n", fails ? "FAILURES" : "ALL OK", cudaGetErrorString(cudaGetLastError()));
   return fails ? 1 : 0;
 }
