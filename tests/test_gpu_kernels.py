@@ -177,3 +177,61 @@ def test_panel_pairs_match_single_panel_steps():
     assert rel_err(np.tril(f2, -1), np.tril(f1, -1)) <= 1e-11
     assert rel_err(res[2][1], res[1][1]) <= 1e-10
     np.testing.assert_allclose(res[2][2], res[1][2], rtol=1e-10)
+
+
+@pytest.mark.parametrize("m,w,nb,side", [(3000, 256, 128, 0), (3000, 200, 128, 1),
+                                         (5000, 100, 128, 0), (1500, 128, 64, 1)])
+def test_panel_block_is_a_block_householder_qr(m, w, nb, side):
+    """qrb_op_panel_block (the multi-GPU step): V (unit lower, in place), the
+    merged T2 and R satisfy (I - V T2 V^T)^T A = [R; 0], with the per-panel T
+    blocks on T2's diagonal; R matches LAPACK up to row signs."""
+    rng = np.random.default_rng(m + w)
+    a = rng.standard_normal((m, w))
+    d, ld = to_dev(a)
+    tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+    tb = torch.zeros(2 * nb * nb, dtype=torch.float64, device="cuda")
+    t2 = torch.zeros((w, w + (w & 1)), dtype=torch.float64, device="cuda")
+    ldt2 = w + (w & 1)
+    assert lib().qrb_op_panel_block(P(d), ld, m, w, nb, P(tau), P(tb), P(t2), ldt2, None,
+                                    side) == 0
+    f = to_host(d, m)
+    T2 = t2.cpu().numpy().T[:w, :w]              # column-major (w x w)
+    v = unit_lower(f)
+    q = np.eye(m) - v @ T2 @ v.T
+    qa = q.T @ a
+    r = np.triu(f[:w])
+    assert np.abs(qa[:w] - r).max() <= 1e-12 * np.abs(a).max() * np.sqrt(m)
+    assert np.abs(qa[w:]).max() <= 1e-12 * np.abs(a).max() * np.sqrt(m)
+    r_ref = sla.qr(a, mode="r")[0][:w]
+    s = np.sign(np.diag(r)) * np.sign(np.diag(r_ref))
+    assert rel_err(r * s[:, None], r_ref) <= 1e-10
+    ta = tb[:nb * nb].view(nb, nb).cpu().numpy().T
+    pa = min(w, nb)
+    assert np.abs(T2[:pa, :pa] - ta[:pa, :pa]).max() <= 1e-14 * max(1.0, np.abs(ta).max())
+
+
+@pytest.mark.parametrize("m,w,nc,split", [(3000, 256, 700, (0, 256, 300)), (2000, 128, 130, (130,)),
+                                          (4000, 512, 900, (512, 100, 288))])
+def test_apply_qt_two_phase_equals_apply_qt(m, w, nc, split):
+    """qrb_op_apply_qt_begin + qrb_op_apply_qt_cols over any column split equals
+    qrb_op_apply_qt bit for bit (the look-ahead's and the multi-GPU owner's
+    update)."""
+    rng = np.random.default_rng(w + nc)
+    vfull = rng.standard_normal((m, w))
+    t = np.triu(rng.standard_normal((w, w))) * 0.01
+    c = rng.standard_normal((m, nc))
+    vd, ldv = to_dev(vfull)
+    td, ldt = to_dev(t)
+    c1, ldc = to_dev(c)
+    c2, _ = to_dev(c)
+    L = lib()
+    assert L.qrb_op_apply_qt(P(vd), ldv, m, w, P(td), ldt, P(c1), ldc, nc, None) == 0
+    assert L.qrb_op_apply_qt_begin(P(vd), ldv, m, w, P(td), ldt, P(c2), ldc, nc, None) == 0
+    c0 = 0
+    for cols in split + (nc - sum(split),):
+        assert L.qrb_op_apply_qt_cols(P(vd), ldv, m, w, P(c2), ldc, c0, cols, None) == 0
+        c0 += cols
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    # columns beyond the last _begin are refused
+    assert L.qrb_op_apply_qt_cols(P(vd), ldv, m, w, P(c2), ldc, nc, 4096, None) != 0
