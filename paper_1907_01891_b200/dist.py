@@ -517,6 +517,10 @@ def bench_rank(args, rank: int, world: int):
 
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
     backend = getattr(args, "dist_backend", "nccl")
+    # NCCL kernels hold one SM per channel while they wait for the owner's block;
+    # a receiver posts its broadcast before its update, so cap the CTAs a
+    # collective may take (the 70 MB block still moves in < 1 ms over NVLink)
+    os.environ.setdefault("NCCL_MAX_CTAS", "8")
     if backend == "gloo":
         # functional check of this multi-rank bench path on a one-GPU box: the
         # ranks share the GPU and exchange through host memory (no performance
