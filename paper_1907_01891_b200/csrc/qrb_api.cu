@@ -84,6 +84,8 @@ struct Workspace {
   DevBuf T2;               // merged block reflector of a panel pair (2nb x 2nb) + scratch
   DevBuf T4;               // scratch of the 4-panel merge (outer_panels = 4)
   int* hflag = nullptr;    // pinned host copy of the status word
+  int64_t w2_cols = 0;     // columns / width of the W2 the last apply_qt_w2 formed
+  int64_t w2_w = 0;
   void release() {
     if (hflag) cudaFreeHost(hflag);
     hflag = nullptr;
@@ -260,6 +262,8 @@ static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const Mat
   const int64_t ldw = even(w);
   QRB_TRY(ws.W.ensure(sizeof(double) * ldw * nc, st));
   QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));
+  ws.w2_cols = nc;
+  ws.w2_w = w;
   const int64_t per_split = ldw * nc;
   const int max_splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(32) << 20) / per_split)));
   const int splits = gemm_pick_splits(w, nc, m, max_splits);
@@ -1656,8 +1660,8 @@ int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, dou
     return QRB_EARG;
   }
   Workspace& ws = device_workspace();
-  if (static_cast<size_t>((c_from + ncols) * even(w)) * sizeof(double) > ws.W2.bytes) {
-    set_last_error("qrb_op_apply_qt_cols: columns beyond the last qrb_op_apply_qt_begin");
+  if (c_from + ncols > ws.w2_cols || w != ws.w2_w) {
+    set_last_error("qrb_op_apply_qt_cols: columns or width beyond the last qrb_op_apply_qt_begin");
     return QRB_EARG;
   }
   return apply_qt_nn(MatView{const_cast<double*>(V), m, w, ldv}, MatView{C, m, c_from + ncols, ldc},
