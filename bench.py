@@ -47,7 +47,6 @@ FP64_PEAK_SOURCE = "measured DMMA peak, profiles/r01_fp64_pipe_probe.log"
 # profiles/r01_fp64_pipe_probe.log)
 FP64_NOMINAL_TFLOPS = 37.2
 CUBLAS_DGEMM_TFLOPS = 35.47
-CPU_SAMPLE_COLS = 1024
 
 
 def qr_flops(m: int, n: int) -> float:
@@ -186,49 +185,132 @@ def measure_config(cfg: int, reps: int = 3) -> dict:
     return out
 
 
-def cpu_sample_tflops(coo, g, steps: int = 1, a_sample=None):
-    """Reference algorithm (oracle port, tiled left-looking QR of oocqr) on the
-    leading m x 1024 column block of A; returns (TFLOP/s, seconds per run)."""
-    from oracle.tiled_qr import factorize_dense
-    ncol = min(CPU_SAMPLE_COLS, g.n_pixels)
-    if a_sample is None:
+# -- CPU reference (oracle port of oocqr's numpy twin), extrapolated to the workload ----------
+
+# reference tile size b: the fastest of b = 1024 / 2048 / 4096 for the reference's own
+# numpy twin on config 3 (profiles/r02_cpu_port_vs_reference.json: 0.137 / 0.127 /
+# 0.035 TFLOP/s extrapolated on 8 build cores; the port is within 10% per task)
+CPU_TILE = 1024
+CPU_INNER = 128      # reference inner block w (EngineConfig.inner_block default)
+
+
+def task_counts(p: int, q: int, r: int) -> dict:
+    """Tasks of the reference's left-looking tiled QR (task_engine.py:187-217) on a
+    p x q tile grid and of its solve (:220-254) with r RHS block columns."""
+    td = sum(p - 1 - k for k in range(q))
+    return {"factor": {"comp_dense_qr": q, "comp_td_qr": td,
+                       "apply_qt_dense": q * (q - 1) // 2,
+                       "apply_qt_td": sum(p - 1 - j for k in range(q) for j in range(k))},
+            "solve": {"apply_qt_dense": q * r, "apply_qt_td": td * r,
+                      "gemm_nn_mo": q * (q - 1) // 2 * r, "trsm_lunn": q * r}}
+
+
+def cpu_tiles(m: int, n: int, b: int, coo=None, a_cols=None):
+    """Two b x b tiles of the workload's A (diagonal tile (0,0) and tile (1,0)),
+    C-ordered like the reference's in-memory tiles (tile_store.py:193-194)."""
+    if a_cols is None:
         r, c, v = coo
-        sel = c < ncol
-        a = np.zeros((g.n_rays, ncol))
-        a[r[sel], c[sel]] = v[sel]
-    else:
-        a = a_sample
-    times = []
+        sel = (c < b) & (r < 2 * b)
+        a_cols = np.zeros((2 * b, b))
+        a_cols[r[sel], c[sel]] = v[sel]
+    blk = np.zeros((2 * b, b))
+    blk[:a_cols.shape[0], :a_cols.shape[1]] = a_cols[:2 * b, :b]
+    return np.ascontiguousarray(blk[:b]), np.ascontiguousarray(blk[b:])
+
+
+def cpu_op_seconds(t0: np.ndarray, t1: np.ndarray, b: int, w: int) -> dict:
+    """One timed execution of each reference tile kernel (oracle port of the
+    numpy twin, kernels.py:296-455) on the workload's own tiles.  The applies
+    reuse the factors the QRs just produced (the reference's data flow)."""
+    from oracle import tiled_qr as orc
+    out = {}
+    a = t0.copy()
+    tic = time.perf_counter()
+    y, s_d = orc.comp_dense_qr(a, w)
+    out["comp_dense_qr"] = time.perf_counter() - tic
+    t, d = y.copy(), t1.copy()
+    tic = time.perf_counter()
+    t, d, s_t = orc.comp_td_qr(t, d, w)
+    out["comp_td_qr"] = time.perf_counter() - tic
+    c = t0.T.copy()                                      # a b x b tile to update
+    tic = time.perf_counter()
+    orc.apply_left_qt_dense(y, s_d, c, w)
+    out["apply_qt_dense"] = time.perf_counter() - tic
+    f, g = t0.T.copy(), t1.T.copy()
+    tic = time.perf_counter()
+    orc.apply_left_qt_td(d, s_t, f, g, w)
+    out["apply_qt_td"] = time.perf_counter() - tic
+    tic = time.perf_counter()
+    orc.gemm_nn_mo(f, t0, g)
+    out["gemm_nn_mo"] = time.perf_counter() - tic
+    rt = np.triu(t) + np.eye(b) * (np.abs(np.diag(t)).max() + 1.0)   # well-posed triangle
+    tic = time.perf_counter()
+    orc.trsm_lunn(rt, g, block=w)
+    out["trsm_lunn"] = time.perf_counter() - tic
+    return out
+
+
+def cpu_extrapolate(op_s: dict, m: int, n: int, slices: int, b: int) -> dict:
+    """Reference time of the whole workload = sum over ops of (task count x
+    measured seconds per task) -- tiles are always full b x b (zero padded,
+    tile_store.py:186-187), so every task of a kind costs the same."""
+    p, q, r = -(-m // b), -(-n // b), -(-slices // b)
+    cnt = task_counts(p, q, r)
+    f_s = sum(cnt["factor"][k] * op_s[k] for k in cnt["factor"])
+    s_s = sum(cnt["solve"][k] * op_s[k] for k in cnt["solve"])
+    return {"factor_s": f_s, "solve_s": s_s, "grid": [p, q, r], "task_counts": cnt,
+            "qr_tflops": qr_flops(m, n) / f_s / 1e12, "slices_per_s": slices / s_s}
+
+
+def cpu_baseline_run(m: int, n: int, slices: int, coo=None, a_cols=None, steps: int = 1,
+                     warmup: int = 0, b: int = CPU_TILE, w: int = CPU_INNER) -> dict:
+    t0, t1 = cpu_tiles(m, n, b, coo, a_cols)
+    for _ in range(warmup):
+        cpu_op_seconds(t0, t1, b, w)
+    runs, wall = [], []
     for _ in range(steps):
-        t0 = time.perf_counter()
-        factorize_dense(a, 1024, 128)
-        times.append(time.perf_counter() - t0)
-    t = float(np.mean(times))
-    return qr_flops(g.n_rays, ncol) / t / 1e12, t, ncol
+        tic = time.perf_counter()
+        runs.append(cpu_op_seconds(t0, t1, b, w))
+        wall.append(time.perf_counter() - tic)
+    op_s = {k: float(np.median([r_[k] for r_ in runs])) for k in runs[0]}
+    ex = cpu_extrapolate(op_s, m, n, slices, b)
+    ex.update({"op_seconds": op_s, "sample_s_per_step": float(np.mean(wall)), "tile": b,
+               "inner_block": w, "cores": len(os.sched_getaffinity(0)),
+               "sample": (f"oracle port of oocqr's numpy twin (OOCQR_DISABLE_NUMBA=1 path): one "
+                          f"execution of each of the 6 tile kernels on the workload's own b={b} "
+                          f"tiles (w={w}) per step, median over {steps} steps; the {m}x{n} QR and "
+                          f"the {slices}-slice solve EXTRAPOLATED as task count x time per task "
+                          f"(grid {-(-m // b)}x{-(-n // b)}, tile I/O excluded, which favours the "
+                          f"reference)")})
+    return ex
 
 
 def reference_arm(args, rank: int):
     if rank != 0:
         return
-    g, coo, _, _ = build_workload(args.config, 1)
     from paper_1907_01891_b200 import ct_system as cs
+    g = cs.config_geometry(args.config)
+    m, n = g.n_rays, g.n_pixels
     S = args.slices or cs.CONFIGS[args.config]["slices"]
-    cores = len(os.sched_getaffinity(0))
-    for _ in range(args.warmup):
-        cpu_sample_tflops(coo, g)
-    val, t, ncol = cpu_sample_tflops(coo, g, steps=args.steps)
+    b = min(CPU_TILE, n)
+    # the two b x b tiles of A the sample runs on: Siddon rays of the first 2b rows
+    r0, c0, v0 = cs.siddon_coo(g)
+    coo = (r0, c0, v0)
+    ex = cpu_baseline_run(m, n, S, coo=coo, steps=args.steps, warmup=args.warmup, b=b)
+    val = ex["qr_tflops"]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Siddon fan-beam A, seeded)",
-        "config": {**workload_config(args.config, g.n_rays, g.n_pixels, S, args.nb),
-                   "sample": f"each step: the reference algorithm (oracle port, tile 1024, "
-                             f"inner block 128) on the leading {g.n_rays}x{ncol} column block "
-                             f"of A; TFLOP/s = 2*m*n^2 - 2n^3/3 of that block / its time"},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
-                                   f"({g.n_rays}x{ncol}), b=1024, w=128"},
+        "ms_per_step": ex["sample_s_per_step"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Siddon fan-beam A, seeded)",
+        "config": workload_config(args.config, m, n, S, args.nb),
+        "extrapolated": True,
+        "reference_factor_s": ex["factor_s"], "reference_solve_s": ex["solve_s"],
+        "slices_per_s": ex["slices_per_s"], "op_seconds": ex["op_seconds"],
+        "task_counts": ex["task_counts"],
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": ex["cores"], "kind": "port",
+                         "sample": ex["sample"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -255,7 +337,7 @@ def ours_arm(args, rank: int, world: int):
     a_dev = cs.densify_device(g, lda)          # sm_100a Siddon kernel, straight into HBM
     torch.cuda.synchronize()
     densify_s = time.perf_counter() - t_setup
-    a_sample = a_dev[:min(CPU_SAMPLE_COLS, n), :m].cpu().numpy().T.copy()
+    cpu_cols = a_dev[:min(CPU_TILE, n), :min(2 * CPU_TILE, m)].cpu().numpy().T.copy()
     # sinograms b = A x + 1% noise (seeded per slice); A x via the device matrix
     xt = torch.from_numpy(np.ascontiguousarray(x_true.T)).cuda()        # (S, n)
     ax_dev = xt @ a_dev[:, :m]                                           # (S, m), noiseless
@@ -309,25 +391,42 @@ def ours_arm(args, rank: int, world: int):
             acc = kstats.setdefault(name, {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
             for key in acc:
                 acc[key] += k[key]
-    dom = max((k for k in kstats if k in ("gemm_tn", "gemm_nn")), key=lambda k: kstats[k]["ms"])
-    dk = kstats[dom]
+    # the dominant kernel by total device time: the trailing-update NN GEMM
+    # (gemm_nn_sub_asyncepi) counts its full-grid launches AND the capped ones
+    # that run beside the look-ahead panel (the same kernel on 148 - la_sms CTAs)
+    zero = {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0}
+    fam = {"gemm_tn": dict(kstats.get("gemm_tn", zero)), "gemm_nn": dict(kstats.get("gemm_nn", zero))}
+    for key in fam["gemm_nn"]:
+        fam["gemm_nn"][key] += kstats.get("gemm_nn_capped", zero)[key]
+    dom = max(fam, key=lambda k: fam[k]["ms"])
+    dk = fam[dom]
     achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": UNIT,
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "kernel": dom,
+                "kernel_name": {"gemm_nn": "gemm_nn_sub_asyncepi (C -= V W2, full-grid + capped "
+                                           "launches)",
+                                "gemm_tn": "gemm_dmma_kernel<KMAJOR=1> (W = V^T C)"}[dom],
                 "peak_source": FP64_PEAK_SOURCE,
                 "per_launch_flops": dk["flops"] / dk["launches"],
-                "avg_launch_ms": dk["ms"] / dk["launches"]}
+                "avg_launch_ms": dk["ms"] / dk["launches"],
+                "time_share": {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4)
+                               for k, v in fam.items()}}
     roofline.update(_ncu_traffic(dom, m, n, args.nb))
     if "gemm_nn_capped" in kstats and kstats["gemm_nn_capped"]["launches"]:
-        ck = kstats["gemm_nn_capped"]
+        ck, uk = kstats["gemm_nn_capped"], kstats["gemm_nn"]
         sms = torch.cuda.get_device_properties(0).multi_processor_count
         la_sms = native.get_tuning("la_sms")
         ca = ck["flops"] / (ck["ms"] * 1e-3) / 1e12
-        # the NN update launched on sms - la_sms CTAs while the next panel pair is
-        # factored on the other SMs (look-ahead); its rate per SM it was given
-        roofline["capped_nn"] = {"achieved": ca, "sms": sms - la_sms,
-                                 "frac_of_its_sms": ca / (FP64_PEAK_TFLOPS * (sms - la_sms) / sms),
-                                 "launches": ck["launches"], "ms": ck["ms"]}
+        ua = uk["flops"] / (uk["ms"] * 1e-3) / 1e12
+        # NN's two launch kinds: whole-GPU rate of the full-grid launches, and the
+        # capped launches' rate per SM they were given (148 - la_sms CTAs while the
+        # next panel pair is factored on the other SMs)
+        roofline["nn_parts"] = {
+            "full_grid": {"achieved": ua, "frac": ua / FP64_PEAK_TFLOPS,
+                          "launches": uk["launches"], "ms": uk["ms"]},
+            "capped": {"achieved": ca, "sms": sms - la_sms,
+                       "frac_of_its_sms": ca / (FP64_PEAK_TFLOPS * (sms - la_sms) / sms),
+                       "launches": ck["launches"], "ms": ck["ms"]}}
     shares = {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4) for k, v in kstats.items()}
     roofline["kernel_tflops"] = {k: round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 3)
                                  for k, v in kstats.items() if v["ms"] > 0 and k.startswith("gemm")}
@@ -427,8 +526,7 @@ def ours_arm(args, rank: int, world: int):
         for c in (1, 2):
             others[f"config{c}"] = measure_config(c)
 
-    cores = len(os.sched_getaffinity(0))
-    cpu_val, cpu_t, ncol = cpu_sample_tflops(None, g, a_sample=a_sample)
+    cpu = cpu_baseline_run(m, n, S, a_cols=cpu_cols, steps=5, warmup=1, b=min(CPU_TILE, n))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -443,9 +541,10 @@ def ours_arm(args, rank: int, world: int):
         "solve_tflops": solve_flops(m, n, S) / (s_ms * 1e-3) / 1e12,
         "factor_ms": f_ms, "solve_ms": s_ms,
         "roofline": roofline, "kernel_time_share": shares,
-        "cpu_baseline": {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"oracle port of oocqr tiled QR on A[:, :{ncol}] "
-                                   f"({m}x{ncol}), b=1024, w=128, {cpu_t:.1f} s"},
+        "cpu_baseline": {"value": cpu["qr_tflops"], "unit": UNIT, "cores": cpu["cores"],
+                         "kind": "port", "sample": cpu["sample"], "extrapolated": True,
+                         "factor_s": cpu["factor_s"], "solve_s": cpu["solve_s"],
+                         "slices_per_s": cpu["slices_per_s"], "op_seconds": cpu["op_seconds"]},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "config5": cfg5, "other_configs": others or None, "quality": quality,
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
@@ -503,6 +602,18 @@ def _ncu_traffic(kernel: str, m: int, n: int, nb: int) -> dict:
             "traffic_algorithmic": algo}
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = {k: v for k, v in os.environ.items() if k != "QRB_JSON_FD"}
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -511,7 +622,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--slices", type=int, default=None)
     ap.add_argument("--nb", type=int, default=128)
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cfg5-slices", type=int, default=4096,
                     help="slices of the config-5 solve-throughput run (0 = skip)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -524,9 +635,15 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start N ranks (one per
+        # GPU) under torch.distributed.run on this node; rank 0 prints the line
+        sys.exit(relaunch_under_torchrun(args.gpus))
     claim_stdout()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         reference_arm(args, rank)
         return

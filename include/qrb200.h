@@ -183,7 +183,11 @@ QRB_API int qrb_op_panel_block(double* A, int64_t lda, int64_t m, int64_t w, int
 /* qrb_op_apply_qt in two phases: _begin forms W2 = T^T V^T C for all nc
  * columns (kept in the library workspace), _cols then applies C -= V W2 to
  * columns [c_from, c_from + ncols) -- so a look-ahead panel can start after the
- * first columns while the rest is updated (on a capped grid, "grid_cap"). */
+ * first columns while the rest is updated (on a capped grid, "grid_cap").
+ * The workspace is per device: _begin and its _cols calls must come from one
+ * host thread, on one stream, with the same V / m / w, and no other W2-forming
+ * call (qrb_solve, qrb_op_apply_qt, qrb_factorize ...) on that device in
+ * between -- _cols checks this and returns QRB_ESTATE otherwise. */
 QRB_API int qrb_op_apply_qt_begin(const double* V, int64_t ldv, int64_t m, int64_t w,
                                   const double* T, int64_t ldt, const double* C, int64_t ldc,
                                   int64_t nc, void* stream);

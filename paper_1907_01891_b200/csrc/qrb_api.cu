@@ -86,6 +86,7 @@ struct Workspace {
   int* hflag = nullptr;    // pinned host copy of the status word
   int64_t w2_cols = 0;     // columns / width of the W2 the last apply_qt_w2 formed
   int64_t w2_w = 0;
+  uint64_t w2_gen = 0;     // bumped by every apply_qt_w2 (qrb_op_apply_qt_cols checks it)
   void release() {
     if (hflag) cudaFreeHost(hflag);
     hflag = nullptr;
@@ -264,6 +265,7 @@ static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const Mat
   QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));
   ws.w2_cols = nc;
   ws.w2_w = w;
+  ++ws.w2_gen;
   const int64_t per_split = ldw * nc;
   const int max_splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(32) << 20) / per_split)));
   const int splits = gemm_pick_splits(w, nc, m, max_splits);
@@ -710,6 +712,15 @@ struct ProfSession {
   }
 };
 
+// everything derived from the factors (R^-1 blocks, merged pair reflectors)
+// must be rebuilt after the matrix or the factors were replaced
+void invalidate_derived(qrb_handle* h) {
+  h->rinv_ready = false;
+  h->t2_ready = false;
+  h->rinv2_ready = false;
+  std::fill(h->t2_valid.begin(), h->t2_valid.end(), 0);
+}
+
 // merged 2nb-wide reflectors of panel pairs (2p, 2p+1), for the solve's Q^T B
 bool pair_ok(const qrb_handle* h, int k) {
   const int64_t j0 = int64_t(k) * h->nb;
@@ -1006,6 +1017,15 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   return QRB_OK;
 }
 
+// what this host thread's last qrb_op_apply_qt_begin formed (checked by _cols)
+struct BeginRecord {
+  uint64_t gen = 0;
+  const void* V = nullptr;
+  int64_t m = 0, w = 0;
+  void* stream = nullptr;
+};
+static thread_local BeginRecord t_begin;
+
 extern "C" {
 
 int qrb_version(void) { return 100; }
@@ -1125,9 +1145,7 @@ int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src
                                  h->stream));
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->factored = false;
-  h->rinv_ready = false;
-  h->t2_ready = false;
-  h->rinv2_ready = false;
+  invalidate_derived(h);
   return QRB_OK;
 }
 
@@ -1151,6 +1169,8 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   clear_report(rep);
   if (!h) return QRB_EARG;
   DeviceGuard g(h->device);
+  h->factored = false;  // until this factorization completes
+  invalidate_derived(h);
   Workspace& ws = device_workspace();
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = h->stream;
@@ -1226,6 +1246,26 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   return QRB_OK;
 }
 
+// Deterministic left-looking -> right-looking switch of qrb_factorize_host: the
+// chunk index at which the modelled compute of the left-looking chunks before it
+// covers the modelled H2D time of the whole matrix (PCIe ~45 GB/s, update
+// ~34 TFLOP/s).  A function of the shape only, so the factors (and their
+// rounding) are the same every run; QRB_E2E_NO_SWITCH keeps the left-looking
+// order to the end.
+static int64_t host_switch_chunk(int64_t m, int64_t n, int64_t W, int64_t nchunks) {
+  static const bool no_switch = std::getenv("QRB_E2E_NO_SWITCH") != nullptr;
+  if (no_switch) return nchunks;
+  const double copy_s = 8.0 * static_cast<double>(m) * n / 45e9;
+  double work_s = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    if (c > 0 && work_s >= copy_s) return c;
+    const double c0 = static_cast<double>(c * W), w = static_cast<double>(std::min(W, n - c * W));
+    // Q^T of the c0 earlier columns on this chunk + the chunk's own QR
+    work_s += (4.0 * m * c0 * w + 2.0 * (m - c0) * w * w) / 34e12;
+  }
+  return nchunks;
+}
+
 int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
                        qrb_report* rep) {
   clear_report(rep);
@@ -1234,6 +1274,8 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     return QRB_EARG;
   }
   DeviceGuard g(h->device);
+  h->factored = false;  // A is overwritten from here on
+  invalidate_derived(h);
   Workspace& ws = device_workspace();
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = h->stream;
@@ -1242,50 +1284,36 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
   if (W == 0) W = 4096;  // measured best at config 3 (2048..32768 swept)
   W = std::max<int64_t>(nb, (W + nb - 1) / nb * nb);
   const int64_t nchunks = (h->n + W - 1) / W;
+  const int64_t c_switch = host_switch_chunk(h->m, h->n, W, nchunks);
   cudaStream_t cs = nullptr;
-  QRB_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   std::vector<cudaEvent_t> landed(nchunks, nullptr);
   cudaEvent_t c0ev = nullptr, c1ev = nullptr;
-  auto cleanup = [&]() {
-    for (auto& e : landed)
-      if (e) cudaEventDestroy(e);
-    if (c0ev) cudaEventDestroy(c0ev);
-    if (c1ev) cudaEventDestroy(c1ev);
-    if (cs) cudaStreamDestroy(cs);
-  };
-  int status = QRB_OK;
-  do {
-    if (cudaEventCreate(&c0ev) != cudaSuccess || cudaEventCreate(&c1ev) != cudaSuccess) {
-      status = QRB_ECUDA;
-      break;
-    }
+  ProfSession session(h);
+  // the whole call; every failure returns through here so the copy stream is
+  // drained and its events released (the caller's src may still be read by it)
+  auto body = [&]() -> int {
+    QRB_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    QRB_CUDA_TRY(cudaEventCreate(&c0ev));
+    QRB_CUDA_TRY(cudaEventCreate(&c1ev));
     // the copy stream starts after everything already queued on the handle's stream
-    cudaEventRecord(h->ev0, st);
-    cudaStreamWaitEvent(cs, h->ev0, 0);
-    cudaEventRecord(c0ev, cs);
+    QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
+    QRB_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev0, 0));
+    QRB_CUDA_TRY(cudaEventRecord(c0ev, cs));
     for (int64_t c = 0; c < nchunks; ++c) {
       const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
-      if (cudaEventCreateWithFlags(&landed[c], cudaEventDisableTiming) != cudaSuccess ||
-          cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double), src + col0 * ld,
-                            ld * sizeof(double), h->m * sizeof(double), nc,
-                            cudaMemcpyHostToDevice, cs) != cudaSuccess ||
-          cudaEventRecord(landed[c], cs) != cudaSuccess) {
-        set_last_error(std::string("qrb_factorize_host: copy: ") +
-                       cudaGetErrorString(cudaGetLastError()));
-        status = QRB_ECUDA;
-        break;
-      }
+      QRB_CUDA_TRY(cudaEventCreateWithFlags(&landed[c], cudaEventDisableTiming));
+      QRB_CUDA_TRY(cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double),
+                                     src + col0 * ld, ld * sizeof(double), h->m * sizeof(double),
+                                     nc, cudaMemcpyHostToDevice, cs));
+      QRB_CUDA_TRY(cudaEventRecord(landed[c], cs));
     }
-    if (status != QRB_OK) break;
-    cudaEventRecord(c1ev, cs);
-    ProfSession session(h);
+    QRB_CUDA_TRY(cudaEventRecord(c1ev, cs));
     MatView A{h->A, h->m, h->n, h->lda};
     QRB_TRY(t2_storage(h));
     // non-finite input check per landed chunk (flag read once at the end)
     QRB_TRY(ws.bar.ensure(64, st));
     int* nf = static_cast<int*>(ws.bar.p) + 8;
     QRB_CUDA_TRY(cudaMemsetAsync(nf, 0, sizeof(int), st));
-    static const bool no_switch = std::getenv("QRB_E2E_NO_SWITCH") != nullptr;
     const int64_t w2 = 2 * int64_t(nb), blk2 = w2 * w2;
     // Q_k^T for every factored panel k < kc0 on the columns C (left-looking):
     // pairs with their merged reflector (K = 2nb GEMMs; the TN runs 35.7 instead
@@ -1305,74 +1333,82 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
       }
       return QRB_OK;
     };
-    for (int64_t c = 0; c < nchunks && status == QRB_OK; ++c) {
+    for (int64_t c = 0; c < nchunks; ++c) {
       const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
-      if (c > 0 && !no_switch && cudaEventQuery(landed[nchunks - 1]) == cudaSuccess) {
-        // the whole matrix has landed: finish in the right-looking order (the
-        // remaining columns catch up on every earlier panel with wide GEMMs,
-        // then the usual panel + trailing-update steps)
+      if (c > 0 && c >= c_switch) {
+        // the rest of the matrix is (modelled to be) on the device: finish in the
+        // right-looking order (the remaining columns catch up on every earlier
+        // panel with wide GEMMs, then the usual panel + trailing-update steps)
         const int64_t rem = h->n - col0;
         QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[nchunks - 1], 0));
         nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, rem, nf);
+        QRB_CUDA_TRY(cudaGetLastError());
         g_launches += 1;
-        status = apply_prev(static_cast<int>(col0 / nb), col0, rem);
-        if (status == QRB_OK) status = right_looking(h, col0, ws, st);
+        QRB_TRY(apply_prev(static_cast<int>(col0 / nb), col0, rem));
+        QRB_TRY(right_looking(h, col0, ws, st));
         break;
       }
       QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[c], 0));
       nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, nc, nf);
+      QRB_CUDA_TRY(cudaGetLastError());
       g_launches += 1;
       // left-looking: every earlier panel applied to this chunk, in order
-      status = apply_prev(static_cast<int>(col0 / nb), col0, nc);
+      QRB_TRY(apply_prev(static_cast<int>(col0 / nb), col0, nc));
       // then the chunk's own panels, right-looking inside the chunk (in pairs)
-      for (int64_t j0 = col0; j0 < col0 + nc && status == QRB_OK; j0 += nb) {
+      for (int64_t j0 = col0; j0 < col0 + nc; j0 += nb) {
         const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
         const int k = static_cast<int>(j0 / nb);
         double* Tk = h->T + int64_t(k) * nb * nb;
         if (g_outer_panels >= 2 && (k & 1) == 0 && j0 + w2 <= col0 + nc && mk >= w2) {
           double* T2 = nullptr;
-          status = factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
-                                     h->T2 + int64_t(k / 2) * blk2);
-          if (status != QRB_OK) break;
+          QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
+                                    h->T2 + int64_t(k / 2) * blk2));
           h->t2_valid[k / 2] = 1;
           const int64_t rest2 = col0 + nc - (j0 + w2);
           if (rest2 > 0)
-            status = apply_qt(A.sub(j0, j0, mk, w2), T2, w2, A.sub(j0, j0 + w2, mk, rest2), ws, st);
+            QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), T2, w2, A.sub(j0, j0 + w2, mk, rest2), ws, st));
           j0 += nb;
           continue;
         }
-        status = factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st);
+        QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st));
         const int64_t rest = col0 + nc - (j0 + pw);
-        if (status == QRB_OK && rest > 0)
-          status = apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, rest), ws, st);
+        if (rest > 0)
+          QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, rest), ws, st));
       }
     }
-    if (status != QRB_OK) break;
     QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
     QRB_CUDA_TRY(cudaEventSynchronize(h->ev1));
     QRB_CUDA_TRY(cudaGetLastError());
-    session.finish(rep);
     int hflag = 0;
     QRB_CUDA_TRY(cudaMemcpy(&hflag, nf, sizeof(int), cudaMemcpyDeviceToHost));
-    h->factored = hflag == 0;
-    h->rinv_ready = false;
-  h->t2_ready = false;
-  h->rinv2_ready = false;
     if (hflag) {
       set_last_error("factorize: input matrix has non-finite entries");
-      status = QRB_ENONFINITE;
-      break;
+      return QRB_ENONFINITE;
     }
+    return QRB_OK;
+  };
+  const int status = body();
+  if (cs) cudaStreamSynchronize(cs);  // no copy from src may outlive the call
+  if (status == QRB_OK) {
+    h->factored = true;
+    session.finish(rep);
     if (rep) {
       const double m = static_cast<double>(h->m), n = static_cast<double>(h->n);
       rep->total_ms = elapsed(h->ev0, h->ev1);
       rep->h2d_ms = elapsed(c0ev, c1ev);
-      rep->h2d_bytes = 8.0 * m * n;
+      rep->h2d_bytes = static_cast<int64_t>(8.0 * m * n);
       rep->flops = 2.0 * m * n * n - 2.0 * n * n * n / 3.0;
       rep->kernel_launches = g_launches.load() - launches0;
     }
-  } while (false);
-  cleanup();
+  } else {
+    cudaStreamSynchronize(st);
+    cudaGetLastError();
+  }
+  for (auto& e : landed)
+    if (e) cudaEventDestroy(e);
+  if (c0ev) cudaEventDestroy(c0ev);
+  if (c1ev) cudaEventDestroy(c1ev);
+  if (cs) cudaStreamDestroy(cs);
   return status;
 }
 
@@ -1400,9 +1436,7 @@ int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t l
                                  cudaMemcpyHostToDevice, h->stream));
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->factored = true;
-  h->rinv_ready = false;
-  h->t2_ready = false;
-  h->rinv2_ready = false;
+  invalidate_derived(h);  // merged pair reflectors of earlier factors are stale
   return QRB_OK;
 }
 
@@ -1648,9 +1682,12 @@ int qrb_op_apply_qt_begin(const double* V, int64_t ldv, int64_t m, int64_t w, co
     return QRB_EARG;
   }
   if (nc == 0) return QRB_OK;
-  return apply_qt_w2(MatView{const_cast<double*>(V), m, w, ldv}, T, ldt,
-                     MatView{const_cast<double*>(C), m, nc, ldc}, device_workspace(),
-                     static_cast<cudaStream_t>(stream));
+  Workspace& ws = device_workspace();
+  QRB_TRY(apply_qt_w2(MatView{const_cast<double*>(V), m, w, ldv}, T, ldt,
+                      MatView{const_cast<double*>(C), m, nc, ldc}, ws,
+                      static_cast<cudaStream_t>(stream)));
+  t_begin = BeginRecord{ws.w2_gen, V, m, w, stream};
+  return QRB_OK;
 }
 
 int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, double* C,
@@ -1663,6 +1700,17 @@ int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, dou
   if (c_from + ncols > ws.w2_cols || w != ws.w2_w) {
     set_last_error("qrb_op_apply_qt_cols: columns or width beyond the last qrb_op_apply_qt_begin");
     return QRB_EARG;
+  }
+  // the W2 in the (per-device) workspace must still be the one this thread's
+  // last _begin formed, for the same reflector block and stream: any other
+  // W2-forming call in between (a solve, qrb_op_apply_qt, another thread)
+  // replaced it
+  if (t_begin.gen != ws.w2_gen || t_begin.V != V || t_begin.m != m || t_begin.w != w ||
+      t_begin.stream != stream) {
+    set_last_error("qrb_op_apply_qt_cols: the workspace W2 is not the one the last "
+                   "qrb_op_apply_qt_begin formed (another W2-forming call ran in between, or "
+                   "a different V / m / stream)");
+    return QRB_ESTATE;
   }
   return apply_qt_nn(MatView{const_cast<double*>(V), m, w, ldv}, MatView{C, m, c_from + ncols, ldc},
                      c_from, ncols, ws, static_cast<cudaStream_t>(stream),

@@ -125,6 +125,13 @@ class QrDevice:
                       "qrb_get_matrix")
         return out
 
+    def get_matrix_device(self, t, col0: int = 0) -> None:
+        """Copy factored columns [col0, col0 + k) into a torch CUDA tensor of
+        shape (k, ld) (column-major m x k, ld >= m), device to device."""
+        ptr, _, cols, ld = colmajor(t)
+        _native.check(self.lib.qrb_get_matrix(self._h, col0, cols, ctypes.c_void_p(ptr), ld, 1),
+                      "qrb_get_matrix")
+
     def r_factor(self) -> np.ndarray:
         return np.triu(self.get_matrix()[: self.n, :])
 

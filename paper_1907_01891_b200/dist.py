@@ -432,7 +432,43 @@ def gather_factored(f: DistFactors, group=None, place=None):
     return full
 
 
-def solve_distributed(f: DistFactors, b_share, ops, group=None):
+def singular_column(diag: np.ndarray, block: int) -> int:
+    """First bad pivot in the reference's bottom-up tile order, or -1
+    (kernels.py:423-426 inside tiles visited from the last, task_engine.py:246-253)."""
+    n = diag.size
+    block = block if block > 0 else max(n, 1)
+    for t in range(-(-n // block) - 1, -1, -1):
+        seg = diag[t * block:min(n, (t + 1) * block)]
+        bad = np.flatnonzero(~(np.abs(seg) >= 1e-300))
+        if bad.size:
+            return t * block + int(bad[0])
+    return -1
+
+
+def global_rdiag(f: DistFactors, group=None) -> np.ndarray:
+    """diag(R) (n values, host) from every rank's factored blocks (one all-reduce)."""
+    import torch
+    import torch.distributed as dist
+    d = torch.zeros(f.n, dtype=torch.float64, device=f.a_local.device)
+    bw = f.block
+    for i, k in enumerate(local_panels(-(-f.n // bw), f.rank, f.world)):
+        c0, w = k * bw, min(bw, f.n - k * bw)
+        cols = torch.arange(w, device=d.device)
+        d[c0:c0 + w] = f.a_local[i * bw + cols, c0 + cols]
+    if f.world > 1:
+        dist.all_reduce(d, group=group)
+    return d.cpu().numpy()
+
+
+def check_singular(f: DistFactors, report_block: int | None = None, group=None) -> None:
+    """Raise SingularMatrixError on EVERY rank with the column the reference's
+    solve would report (tiles of report_block visited bottom-up)."""
+    bad = singular_column(global_rdiag(f, group), report_block or f.n)
+    if bad >= 0:
+        raise SingularMatrixError(bad)
+
+
+def solve_distributed(f: DistFactors, b_share, ops, group=None, report_block: int | None = None):
     """Memory-lean multi-GPU solve (no factor replication; config 4 at 8 GPUs):
     every rank keeps only its own panels and solves its slice share b_share
     (torch (s, lda), s may be 0).
@@ -448,6 +484,7 @@ def solve_distributed(f: DistFactors, b_share, ops, group=None):
     import torch.distributed as dist
 
     m, n, nb, lda, rank, world = f.m, f.n, f.nb, f.lda, f.rank, f.world
+    check_singular(f, report_block, group)          # before any work (reference order)
     npan = -(-n // nb)
     dev = f.a_local.device
     s = b_share.shape[0]
@@ -476,10 +513,6 @@ def solve_distributed(f: DistFactors, b_share, ops, group=None):
             rblk[:, :i1].copy_(f.a_local[lcol:lcol + bs, :i1])
         if world > 1:
             dist.broadcast(rblk, src=own, group=group)
-        diag = torch.diagonal(rblk[:, i0:i1]).cpu().numpy()
-        bad = np.flatnonzero(~(np.abs(diag) >= 1e-300))
-        if bad.size:
-            raise SingularMatrixError(i0 + int(bad[0]))
         if s:
             ops.trsm_upper(rblk, ldr, i0, bs, y, lda, i0, s)
             if i0 > 0:
@@ -683,27 +716,39 @@ def bench_rank(args, rank: int, world: int):
     if rank == 0:
         fl = qr_flops(m, n)
         value = fl / float(f_s) / 1e12
+        n_dev = min(world, torch.cuda.device_count())
+        if backend == "gloo":
+            # functional mode: the ranks share the box's GPU(s) and exchange
+            # through host memory -- not a multi-GPU measurement
+            parallelism = (f"FUNCTIONAL CHECK, not a multi-GPU measurement: {world} ranks sharing "
+                           f"{n_dev} GPU(s), gloo (host-mediated) block broadcast, 1D block-cyclic "
+                           f"column blocks of {bw}; slices split for the solve")
+        else:
+            parallelism = (f"1D block-cyclic column blocks of {bw} (panel pairs, nb={nb}) over "
+                           f"{world} GPUs, NCCL block broadcast, owner look-ahead on a side "
+                           f"stream; slices split for the solve")
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_dev, "ranks": world,
+            "backend": backend, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(step_ms), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Siddon fan-beam A, seeded phantoms, 1% noise)",
             "config": {"workload": f"config{args.config}: QR of A {m}x{n} + solve {S} slices",
-                       "parallelism": f"1D block-cyclic column blocks of {bw} (panel pairs, nb={nb}) "
-                                      f"over {world} GPUs, NCCL block broadcast, owner "
-                                      f"look-ahead on a side stream; slices split for the solve"},
-            "pct_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
-            "pct_fp64_nominal": value / (FP64_NOMINAL_TFLOPS * world),
-            "vs_cublas_dgemm": value / (CUBLAS_DGEMM_TFLOPS * world),
+                       "m": m, "n": n, "slices": S, "panel_width": nb,
+                       "parallelism": parallelism,
+                       "l2": "inputs (A = %.1f GB) larger than L2 (126 MB)" % (m * n * 8 / 1e9)},
+            "pct_fp64_peak": value / (FP64_PEAK_TFLOPS * n_dev),
+            "pct_fp64_nominal": value / (FP64_NOMINAL_TFLOPS * n_dev),
+            "vs_cublas_dgemm": value / (CUBLAS_DGEMM_TFLOPS * n_dev),
             "slices_per_s": S / float(s_s),
             "solve_tflops": solve_flops(m, n, S) / float(s_s) / 1e12,
             "factor_ms": float(f_s) * 1e3, "gather_ms": float(np.mean(gs)) * 1e3,
             "solve_path": "streamed V/R broadcast (no replication)" if lean else
                           "all-gathered factors, per-rank solve",
             "gpu_launches": int(launches), "clocks": clocks,
-            "roofline": {"bound": "tensor", "achieved": value / world,
+            "roofline": {"bound": "tensor", "achieved": value / n_dev,
                          "peak": FP64_PEAK_TFLOPS, "unit": UNIT,
-                         "frac": value / world / FP64_PEAK_TFLOPS, "traffic": None,
+                         "frac": value / n_dev / FP64_PEAK_TFLOPS, "traffic": None,
                          "kernel": "whole factorization per GPU (CUDA events, max over "
                                    "ranks); per-kernel accounting is single-GPU only"},
             "config5": cfg5,

@@ -30,6 +30,7 @@ from pathlib import Path
 
 import numpy as np
 
+from . import dist_api
 from .device import QrDevice
 from .errors import (CacheCapacityError, CorruptTileError, MissingFactorsError,
                      SingularMatrixError, TaskIoError)
@@ -65,6 +66,11 @@ class EngineConfig:
     panel_width: int = 128
     device: int = 0
     hbm_budget_bytes: int = 0  # 0 = 85% of free HBM; above it A is host-staged (ooc.py)
+    # GPUs (= ranks of the torch.distributed process group, one process per GPU,
+    # every rank calling factorize/solve with the same arguments -- dist_api.py):
+    # 0 = the initialized process group's size (1 without one), 1 = this process's
+    # GPU only, N > 1 = require a group of N ranks
+    world_size: int = 0
 
     def validate(self) -> "EngineConfig":
         if self.tile_size < 1:
@@ -88,6 +94,8 @@ class EngineConfig:
                              f"got {self.panel_width}")
         if self.hbm_budget_bytes < 0:
             raise ValueError("hbm_budget_bytes must be >= 0")
+        if self.world_size < 0:
+            raise ValueError(f"world_size must be >= 0, got {self.world_size}")
         return self
 
     def min_cache_tiles(self) -> int:
@@ -125,6 +133,7 @@ class RunReport:
     gpu_flops: float = 0.0
     h2d_seconds: float = 0.0
     d2h_seconds: float = 0.0
+    world_size: int = 1          # GPUs (ranks) the call ran on
 
     @property
     def gpu_tflops(self) -> float:
@@ -169,6 +178,8 @@ class QrFactors:
     directory: Path | None = None
     device_state: QrDevice | None = field(default=None, repr=False, compare=False)
     host_state: object = field(default=None, repr=False, compare=False)  # ooc.HostStagedQR
+    # (dist.DistFactors, local blocks) of this rank after a distributed factorize
+    dist_state: object = field(default=None, repr=False, compare=False)
 
     @property
     def grid_rows(self) -> int:
@@ -387,6 +398,9 @@ def factorize(a: TiledMatrix, config: EngineConfig, factors_dir,
         raise ValueError(f"config tile_size {cfg.tile_size} != matrix tile_size {a.tile_size}")
     factors_dir = Path(factors_dir)
     factors_dir.mkdir(parents=True, exist_ok=True)
+    ctx = dist_api.context(cfg)
+    if ctx is not None:                      # one process per GPU, block-cyclic columns
+        return dist_api.factorize(a, cfg, factors_dir, geometry_hash, *ctx)
     if not _fits_in_hbm(a.rows, a.cols, cfg):
         if _fits_in_host(a.rows, a.cols, cfg):
             return _factorize_host_staged(a, cfg, factors_dir, geometry_hash)
@@ -455,6 +469,9 @@ def solve(factors: QrFactors, b_mat: TiledMatrix, config: EngineConfig,
     factors.check_complete()
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
+    ctx = dist_api.context(cfg)
+    if ctx is not None:                      # slices split over the ranks
+        return dist_api.solve(factors, b_mat, cfg, out_dir, *ctx)
     if factors.host_state is not None or (factors.device_state is None and
                                           not _fits_in_hbm(factors.rows, factors.cols, cfg)):
         return _solve_host_staged(factors, b_mat, cfg, out_dir)

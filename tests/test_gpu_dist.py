@@ -56,28 +56,42 @@ def test_single_rank_nccl_factor_gather_solve():
         dist.destroy_process_group()
 
 
-def test_bench_multirank_path_two_ranks_gloo(tmp_path):
+def _bench_line(cmd, root):
+    import json
+    import subprocess
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    return json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+
+
+@pytest.mark.parametrize("launcher", ["torchrun", "self"])
+def test_bench_multirank_path_two_ranks_gloo(tmp_path, launcher):
     """bench.py's multi-GPU path (dist.bench_rank: per-rank Siddon densify,
     all-reduced sinograms, block-cyclic factorization with the owner's side-
     stream look-ahead, gather, slice-split solve, e2e) end to end with 2 ranks
-    under torchrun -- here over gloo with both ranks on the one GPU, so the
-    control flow of an N = 2 run is exercised (not its performance)."""
-    import json
-    import subprocess
+    -- under torchrun, and as `python bench.py --gpus 2` with no launcher (the
+    script starts its ranks itself) -- here over gloo with both ranks on the one
+    GPU, so the control flow of an N = 2 run is exercised (not its
+    performance; the line says so: "ranks" 2, "n_gpus" = GPUs actually used)."""
     import sys
     from pathlib import Path
 
+    import torch
     root = Path(__file__).resolve().parent.parent
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
-           "--gpus", "2", "--config", "2", "--dist-backend", "gloo", "--steps", "1",
-           "--warmup", "1"]
-    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
-    assert res.returncode == 0, res.stderr[-3000:]
-    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    args = ["--gpus", "2", "--config", "2", "--dist-backend", "gloo", "--steps", "1",
+            "--warmup", "1"]
+    if launcher == "torchrun":
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+               "2", "--master-addr", "127.0.0.1", "--master-port", str(port),
+               str(root / "bench.py"), *args]
+    else:
+        cmd = [sys.executable, str(root / "bench.py"), *args]
+    line = _bench_line(cmd, root)
+    assert line["ranks"] == 2 and line["n_gpus"] == min(2, torch.cuda.device_count())
+    assert line["backend"] == "gloo" and "FUNCTIONAL CHECK" in line["config"]["parallelism"]
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["slices_per_s"] > 0 and line["gpu_launches"] > 0

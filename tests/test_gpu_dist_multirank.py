@@ -101,3 +101,58 @@ def test_multirank_cuda_schedule_matches_oracle(tmp_path, world, m, n, nb, la, b
         assert rel_err(x2, x_ref[:, first:first + cnt]) <= 1e-8
         np.testing.assert_allclose(np.load(tmp_path / f"r2_{rank}.npy"), r_ref[first:first + cnt],
                                    rtol=1e-9)
+
+
+def _dropin_worker(rank, world, port, root, m, n, b, nb):
+    import torch.distributed as dist
+
+    import paper_1907_01891_b200 as pkg
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK="0")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = pkg.EngineConfig(tile_size=b, inner_block=128, panel_width=nb)   # world_size 0: auto
+        a = pkg.TiledMatrix.open(os.path.join(root, "a"))
+        bm = pkg.TiledMatrix.open(os.path.join(root, "b"))
+        factors, rep = pkg.factorize(a, cfg, os.path.join(root, "f"))
+        assert rep.world_size == world and factors.dist_state is not None
+        pkg.solve(factors, bm, cfg, os.path.join(root, "out"))
+        # a later process: solve from the directory (each rank re-reads its blocks)
+        f2 = pkg.QrFactors.load(os.path.join(root, "f"))
+        pkg.solve(f2, bm, cfg, os.path.join(root, "out2"))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,n,b,nb", [(2, 1500, 1100, 512, 64), (3, 900, 700, 256, 32)])
+def test_dropin_factorize_solve_routes_to_block_cyclic_ranks(tmp_path, world, m, n, b, nb):
+    """The reference API itself (factorize / solve) called by every rank of a
+    process group: routed to dist_api (block-cyclic factorization with the CUDA
+    kernels, slice-split solve, every rank writing its own columns of the
+    stores); the result is the single-process oracle's."""
+    import torch.multiprocessing as mp
+
+    import paper_1907_01891_b200 as pkg
+    from oracle import tiled_qr as orc
+    rng = np.random.default_rng(23)
+    a = rng.standard_normal((m, n))
+    bmat = rng.standard_normal((m, 5))
+    pkg.scatter_matrix(pkg.TiledMatrix.create(m, n, b, tmp_path / "a"), a)
+    pkg.scatter_matrix(pkg.TiledMatrix.create(m, 5, b, tmp_path / "b"), bmat)
+    mp.spawn(_dropin_worker, args=(world, _free_port(), str(tmp_path), m, n, b, nb),
+             nprocs=world, join=True)
+    f = orc.factorize_dense(a, 128, 32)
+    fact = pkg.gather_matrix(pkg.TiledMatrix.open(tmp_path / "f" / "factored"))
+    r, r_ref = np.triu(fact[:n]), f.r()
+    s = np.sign(np.diag(r)) * np.sign(np.diag(r_ref))
+    assert np.abs(r * s[:, None] - r_ref).max() <= 1e-10 * np.abs(r_ref).max()
+    x_ref = orc.solve_dense(f, bmat)
+    for out in ("out", "out2"):
+        x = pkg.gather_matrix(pkg.TiledMatrix.open(tmp_path / out / "x"))
+        assert np.abs(x - x_ref).max() <= 1e-8 * np.abs(x_ref).max()
+    # the factors directory is the single-GPU format: one process solves from it too
+    x1 = pkg.solve(pkg.QrFactors.load(tmp_path / "f"), pkg.TiledMatrix.open(tmp_path / "b"),
+                   pkg.EngineConfig(tile_size=b, panel_width=nb, world_size=1), tmp_path / "o1")[0]
+    assert np.abs(pkg.gather_matrix(x1) - x_ref).max() <= 1e-8 * np.abs(x_ref).max()

@@ -266,3 +266,47 @@ def test_lookahead_factorization_matches_oracle_and_is_deterministic(m, n, outer
         for k, v in keys.items():
             _native.set_tuning(k, v)
         torch.cuda.synchronize()
+
+
+def test_reloaded_handle_rebuilds_merged_reflectors():
+    """A handle that already solved (so its merged 2nb panel-pair reflectors
+    are built) and is then reloaded with set_matrix + set_factors of ANOTHER
+    matrix must solve against the new factors, not reuse the old pairs."""
+    rng = np.random.default_rng(11)
+    m, n = 1500, 1024
+    a1 = rng.standard_normal((m, n))
+    a2 = rng.standard_normal((m, n))
+    b = rng.standard_normal((m, 3))
+    with gpu_qr(a2) as q2:
+        f2, (tau2, t2) = q2.get_matrix(), q2.factors()
+        x2_ref, _, _ = q2.solve(b)
+    with gpu_qr(a1) as q:
+        q.solve(b)                                  # builds the merged pair reflectors of a1
+        q.set_matrix(f2)
+        q.set_factors(tau2, t2)
+        x, _, _ = q.solve(b)
+    assert rel_err(x, x2_ref) <= 1e-13
+    x_np = np.linalg.lstsq(a2, b, rcond=None)[0]
+    assert rel_err(x, x_np) <= X_TOL
+
+
+def test_apply_qt_cols_rejects_a_replaced_workspace():
+    """qrb_op_apply_qt_cols refuses to apply a W2 that another W2-forming call
+    replaced after qrb_op_apply_qt_begin (the per-device workspace is shared)."""
+    import ctypes
+
+    import torch
+    from paper_1907_01891_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(5)
+    m, w, nc = 512, 64, 96
+    v = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((w, m)))).cuda()
+    t = torch.from_numpy(np.ascontiguousarray(np.triu(rng.standard_normal((w, w))))).cuda()
+    c = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((nc, m)))).cuda()
+    p = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+    assert lib.qrb_op_apply_qt_begin(p(v), m, m, w, p(t), w, p(c), m, nc, None) == 0
+    assert lib.qrb_op_apply_qt_cols(p(v), m, m, w, p(c), m, 0, 32, None) == 0
+    c2 = c.clone()
+    assert lib.qrb_op_apply_qt(p(v), m, m, w, p(t), w, p(c2), m, nc, None) == 0   # new W2
+    assert lib.qrb_op_apply_qt_cols(p(v), m, m, w, p(c), m, 32, 32, None) == _native.QRB_ESTATE
+    torch.cuda.synchronize()
