@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (BN / 2);
-  int kit = 0;
+  int s = 0;  // ring position carried across work units
+  uint32_t ph = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     int m_tile, n_tile, split;
     decode(u, m_tile, n_tile, split);
@@ -210,6 +211,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int num_k = (k_end - k_begin + BK - 1) / BK;
     const int mg0 = m_tile * BM;
     const int ng0 = n_tile * BN;
+    // K-slice ranges that touch a unit-lower (masked) block, as per-unit bounds:
+    // K-major A / B are masked while kg0 <= (first row of the tile) + rows - 1,
+    // an M-major A from kg0 >= mg0 - BK + 1 on
+    auto last_masked = [&](int lim) { return lim < k_begin ? 0 : (lim - k_begin) / BK + 1; };
+    const int ka_lo = A_KMAJOR ? 0 : (mg0 - BK + 1 <= k_begin ? 0 : (mg0 - k_begin) / BK);
+    const int ka_hi = !args.mask_a ? 0 : A_KMAJOR ? last_masked(mg0 + BM - 1) : num_k;
+    const int kb_hi = args.mask_b ? last_masked(ng0 + BN - 1) : 0;
 
     double acc[4][NT][2];
 #pragma unroll
@@ -217,17 +225,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < num_k; ++kt, ++kit) {
-      const int s = kit % STAGES;
-      mbar_wait(&full[s], (kit / STAGES) & 1);
+    for (int kt = 0; kt < num_k; ++kt) {
+      mbar_wait(&full[s], ph);
       const uint8_t* sA = smem + s * STAGE_BYTES;
       const uint8_t* sB = sA + A_BYTES;
       const int kg0 = k_begin + kt * BK;
-      bool ma = false, mb = false;
-      if (args.mask_a) {
-        ma = A_KMAJOR ? (kg0 <= mg0 + BM - 1) : (mg0 <= kg0 + BK - 1);
-      }
-      if (args.mask_b) mb = (kg0 <= ng0 + BN - 1);
+      const bool ma = kt >= ka_lo && kt < ka_hi;
+      const bool mb = kt < kb_hi;
       if (ma || mb) {
         if (ma && mb)
           consume_stage<A_KMAJOR, BN, true, true>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
@@ -240,6 +244,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == STAGES) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
 
     // ---------------- epilogue ----------------
@@ -328,6 +336,10 @@ struct NnArgs {
   int num_tiles;
   int* counter;  // dynamic tile scheduler (async-epilogue kernel); nullptr = static
 };
+
+__device__ __forceinline__ double neg_bits(double x) {
+  return __hiloint2double(__double2hiint(x) ^ static_cast<int>(0x80000000u), __double2loint(x));
+}
 
 __device__ __forceinline__ void decode_tile(int tile, int num_m, int num_n, int group_m,
                                             int& m_tile, int& n_tile) {
@@ -605,9 +617,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 // releasing the buffer when the bulk reads are done.  The consumers go straight
 // back to the DMMA main loop of the next tile (no named barrier in their path).
 // ---------------------------------------------------------------------------
-constexpr int AE_STAGES = 6;
+#ifndef QRB_NN_STAGES
+#define QRB_NN_STAGES 6
+#endif
+constexpr int AE_STAGES = QRB_NN_STAGES;
 #ifndef QRB_NN_STAGGER_NS
-#define QRB_NN_STAGGER_NS 4000
+#define QRB_NN_STAGGER_NS 0
 #endif
 constexpr int AE_SBUF = 1;  // staging buffers (the bulk read of one finishes long before the next tile)
 constexpr int AE_THREADS = (CONSUMER_WARPS + 2) * 32;  // + producer warp + epilogue warp
@@ -701,40 +716,51 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   }
 
   // ---- consumer warps: DMMA main loop, stage -acc, arrive ----
-  // Warps 4-7 start a few microseconds after warps 0-3 (which share their
-  // SMSPs) and stay behind by up to the ring depth, so the two warps of an
-  // SMSP reach the tile epilogue (staging -acc through shared memory) at
-  // different times and the DMMA pipe stays fed by the other one (tools/gemm_k.py,
-  // K = 256: 34.75 -> 34.96 TFLOP/s; flat for 4-24 us.  A barrier-enforced lag
-  // of 2-5 ring stages measured 34.34-34.43, i.e. worse).
+  // Loop bookkeeping is kept off the DMMA warps' issue path: the ring position
+  // (stage, parity) is carried across tiles instead of kit % 6 / kit / 6, the
+  // V-mask test is one compare against a per-tile bound, and -acc is formed by
+  // flipping sign bits on the integer pipe (a DADD shares the FP64 pipe with
+  // DMMA).  r02 (tools/nn_variants.py, 69120 x 32768): K = 256 34.87 -> 35.84,
+  // K = 512 35.37 -> 36.04 TFLOP/s.  With that, the r01 stagger of warps 4-7
+  // (QRB_NN_STAGGER_NS, which made them hold ring stages the leading warps were
+  // waiting for) no longer pays: 0 / 2 / 4 / 8 us = 35.84 / 35.79 / 35.37 / 35.37
+  // at K = 256, so it is off by default.
   const int g = lane >> 2;
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (NN_BN / 2);
-  int kit = 0, it = 0;
+  int it = 0;
+  // ring position (stage, parity) carried across tiles: no divisions in the loop
+  int s = 0;
+  uint32_t ph = 0;
   if (QRB_NN_STAGGER_NS > 0 && warp >= CONSUMER_WARPS / 2) __nanosleep(QRB_NN_STAGGER_NS);
   for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
     int m_tile, n_tile;
     decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
     const int mg0 = m_tile * BM;
     const int ng0 = n_tile * NN_BN;
+    // K slices from kt_mask on touch the unit-lower block of V (rows mg0.. <= k)
+    const int kt_mask = args.mask_a ? mg0 / BK : num_k;
     double acc[4][NT][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kt = 0; kt < num_k; ++kt, ++kit) {
-      const int s = kit % AE_STAGES;
-      mbar_wait(&full[s], (kit / AE_STAGES) & 1);
+    for (int kt = 0; kt < num_k; ++kt) {
+      mbar_wait(&full[s], ph);
       const uint8_t* sA = smem + s * NN_STAGE_BYTES;
       const uint8_t* sB = sA + NN_A_BYTES;
       const int kg0 = kt * BK;
-      if (args.mask_a && mg0 <= kg0 + BK - 1)
+      if (kt >= kt_mask)
         consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
       else
         consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == AE_STAGES) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
     const int sb = it % AE_SBUF;
     if (it >= AE_SBUF) mbar_wait(&sempty[sb], ((it / AE_SBUF) - 1) & 1);
@@ -747,8 +773,10 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = n0 + nt * 8 + rp(2 * q + e);
+          // -acc by flipping the sign bits on the integer pipe (a DADD would
+          // occupy the FP64 pipe the DMMAs share)
           *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
-              make_double2(-acc[mp * 2 + 0][nt][e], -acc[mp * 2 + 1][nt][e]);
+              make_double2(neg_bits(acc[mp * 2 + 0][nt][e]), neg_bits(acc[mp * 2 + 1][nt][e]));
         }
       }
     }
@@ -880,14 +908,12 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
   const int q = lane & 3;
   const int m0 = (warp & 3) * 32;
   const int n0 = (warp >> 2) * (NN_BN / 2);
-  int kit = 0;
+  int s = 0;  // ring position carried across tiles (no divisions in the loop)
+  uint32_t ph = 0;
   for (int it = 0;; ++it) {
     // the tile id arrives with the first ring stage of the tile
-    {
-      const int s0 = kit % AE_STAGES;
-      mbar_wait(&full[s0], (kit / AE_STAGES) & 1);
-    }
-    const int tile = stage_tile[kit % AE_STAGES];
+    mbar_wait(&full[s], ph);
+    const int tile = stage_tile[s];
     if (tile < 0) {
       // pass the end marker on to the epilogue warp (after its last staging)
       const int sb = it % AE_SBUF;
@@ -901,23 +927,27 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
     decode_tile(tile, num_m, num_n, args.group_m, m_tile, n_tile);
     const int mg0 = m_tile * BM;
     const int ng0 = n_tile * NN_BN;
+    const int kt_mask = args.mask_a ? mg0 / BK : num_k;
     double acc[4][NT][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int kt = 0; kt < num_k; ++kt, ++kit) {
-      const int s = kit % AE_STAGES;
-      mbar_wait(&full[s], (kit / AE_STAGES) & 1);
+    for (int kt = 0; kt < num_k; ++kt) {
+      if (kt > 0) mbar_wait(&full[s], ph);  // (the first stage was waited for above)
       const uint8_t* sA = smem + s * NN_STAGE_BYTES;
       const uint8_t* sB = sA + NN_A_BYTES;
       const int kg0 = kt * BK;
-      if (args.mask_a && mg0 <= kg0 + BK - 1)
+      if (kt >= kt_mask)
         consume_stage<false, NN_BN, true, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
       else
         consume_stage<false, NN_BN, false, false>(acc, sA, sB, m0, n0, g, q, kg0, mg0, ng0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == AE_STAGES) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
     const int sb = it % AE_SBUF;
     if (it >= AE_SBUF) mbar_wait(&sempty[sb], ((it / AE_SBUF) - 1) & 1);
@@ -931,7 +961,7 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           const int n = n0 + nt * 8 + rp(2 * q + e);
           *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
-              make_double2(-acc[mp * 2 + 0][nt][e], -acc[mp * 2 + 1][nt][e]);
+              make_double2(neg_bits(acc[mp * 2 + 0][nt][e]), neg_bits(acc[mp * 2 + 1][nt][e]));
         }
       }
     }

@@ -521,6 +521,34 @@ def solve_distributed(f: DistFactors, b_share, ops, group=None, report_block: in
     return y[:, :n], resid
 
 
+def memory_plan(m: int, n: int, nb: int, world: int, hbm_bytes: float, bw: int | None = None,
+                headroom: float = 0.8) -> dict:
+    """Per-rank HBM plan of the multi-GPU factorization + solve (bytes).
+
+    local: this layout's largest local share of A (column blocks of bw = 2 nb,
+    block k on rank k % world); bcast: the two alternating (V, T2, tau) block
+    buffers of factorize_distributed; t_tau: T of every panel + tau; replica:
+    what the replicated solve adds (a full QrDevice copy of the factors plus
+    gather_factored's all-gather receive buffer).  The solve replicates only if
+    local + bcast + t_tau + replica fits ``headroom`` of the HBM, otherwise it is
+    the memory-lean streamed solve (solve_distributed).
+    """
+    bw = bw or 2 * nb
+    lda = (m + 31) // 32 * 32
+    max_local = max(local_cols(n, bw, r, world) for r in range(world))
+    local = 8.0 * lda * max_local
+    bcast_each = 8.0 * ((m + (m & 1)) * bw + bw * bw + bw)
+    npan = -(-n // nb)
+    t_tau = 8.0 * (npan * nb * nb + npan * nb)
+    replica = 8.0 * lda * n + 8.0 * world * max_local * lda
+    base = local + 2 * bcast_each + t_tau
+    lean = base + replica > headroom * hbm_bytes
+    return {"lda": lda, "block_width": bw, "local_cols": max_local, "local_bytes": local,
+            "bcast_buffer_bytes": bcast_each, "bcast_buffers": 2, "t_tau_bytes": t_tau,
+            "replica_bytes": replica, "total_bytes": base + (0.0 if lean else replica),
+            "lean_solve": lean, "fits": base <= headroom * hbm_bytes}
+
+
 def scatter_block_cyclic(a_full_cols, n: int, nb: int, rank: int, world: int):
     """This rank's local panels (torch (n_local, lda)) from a full (n, lda) tensor."""
     import torch
@@ -607,7 +635,8 @@ def bench_rank(args, rank: int, world: int):
     # replicate the factors for the solve only if a full copy (plus the gather
     # buffer) fits next to the local panels; otherwise stream V and R (config 4)
     free, total = torch.cuda.mem_get_info()
-    lean = args.lean_solve or 2 * 8 * lda * n > 0.8 * free
+    plan = memory_plan(m, n, nb, world, free + 8.0 * a_local.numel(), bw=bw)
+    lean = args.lean_solve or plan["lean_solve"]
     q = None if lean else QrDevice(m, n, nb)
 
     def step():

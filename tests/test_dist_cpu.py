@@ -155,3 +155,20 @@ def test_ownership_helpers():
     assert sum(qd.local_cols(1000, 128, r, 3) for r in range(3)) == 1000
     shares = [qd.slice_share(4096, r, 8) for r in range(8)]
     assert shares[0] == (0, 512) and sum(c for _, c in shares) == 4096
+
+
+def test_config4_memory_plan_at_8_gpus():
+    """BASELINE config 4 (270000 x 262144 fp64, 566 GB) on 8 x B200 (180 GB):
+    ~71 GB of A per rank, two ~553 MB block-broadcast buffers, and no room for
+    a replica of the factors, so the solve is the memory-lean streamed one;
+    config 3 (36 GB) replicates."""
+    hbm = 179e9
+    p = qd.memory_plan(270000, 262144, 128, 8, hbm)
+    assert p["local_cols"] == 32768
+    assert abs(p["local_bytes"] - 70.8e9) < 0.1e9
+    assert p["bcast_buffers"] == 2 and abs(p["bcast_buffer_bytes"] - 553.5e6) < 1e6
+    assert p["fits"] and p["lean_solve"] and p["total_bytes"] < 75e9
+    p3 = qd.memory_plan(69120, 65536, 128, 8, hbm)
+    assert not p3["lean_solve"] and p3["fits"]
+    # one GPU cannot hold config 4 at all (the host-staged tier takes over)
+    assert not qd.memory_plan(270000, 262144, 128, 1, hbm)["fits"]
