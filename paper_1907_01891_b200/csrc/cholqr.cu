@@ -375,15 +375,32 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
   if (t == 0 && sb.bad) atomicOr(flag, bit);
 }
 
-// P[0:b, 0:b] <- S R (on/above the diagonal) and L1 (below); tau_k = T_kk
+// P[0:b, 0:b] <- S R (on/above the diagonal) and L1 (below); tau_k = T_kk;
+// Tout <- T.  Runs only when the chain's flag is clear; otherwise it counts the
+// panel as a Householder fallback (the predicated fallback kernels follow).
+__device__ unsigned long long g_cholqr_fallback_count = 0;
+
 __global__ void cholqr_write_top_kernel(double* P, int64_t ldp, int b, const double* R,
                                         const double* s, const double* L1, const double* T,
-                                        int64_t ldt, double* tau, int ldo) {
+                                        int64_t ldt, double* tau, int ldo, double* Tout,
+                                        int64_t ldto, const int* flag) {
+  if (*reinterpret_cast<const volatile int*>(flag) != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_cholqr_fallback_count, 1ull);
+    return;
+  }
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= b * b) return;
   const int c = idx / b, r = idx - c * b;
   P[r + c * ldp] = r <= c ? s[r] * R[r + (int64_t)c * ldo] : L1[r + (int64_t)c * ldo];
-  if (r == c) tau[c] = T[c + c * ldt];
+  const double tv = T[r + c * ldt];
+  Tout[r + c * ldto] = tv;
+  if (r == c) tau[c] = tv;
+}
+
+// graph capture: the CholeskyQR2 panel's IF node takes the Householder branch
+// when the chain raised its flag
+__global__ void set_conditional_kernel(cudaGraphConditionalHandle h, const int* flag) {
+  cudaGraphSetConditional(h, *reinterpret_cast<const volatile int*>(flag) != 0 ? 1u : 0u);
 }
 
 size_t sd_smem(int) { return (size_t)NP * (NP + 1) * sizeof(double); }
@@ -424,12 +441,25 @@ int modified_lu(const double* Qt, int ldq, int b, double* Uc, double* NUcS, doub
 
 int cholqr_write_top(double* P, int64_t ldp, int b, const double* R, const double* s,
                      const double* L1, const double* T, int64_t ldt, double* tau, int ldo,
-                     cudaStream_t stream) {
+                     double* Tout, int64_t ldto, const int* flag, cudaStream_t stream) {
   const int total = b * b;
   cholqr_write_top_kernel<<<(total + 255) / 256, 256, 0, stream>>>(P, ldp, b, R, s, L1, T, ldt,
-                                                                   tau, ldo);
+                                                                   tau, ldo, Tout, ldto, flag);
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
+}
+
+int set_conditional_from_flag(cudaGraphConditionalHandle h, const int* flag,
+                              cudaStream_t stream) {
+  set_conditional_kernel<<<1, 1, 0, stream>>>(h, flag);
+  QRB_CUDA_TRY(cudaGetLastError());
+  return QRB_OK;
+}
+
+int64_t cholqr_fallback_count() {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_cholqr_fallback_count, sizeof(v)) != cudaSuccess) return -1;
+  return static_cast<int64_t>(v);
 }
 
 }  // namespace qrb

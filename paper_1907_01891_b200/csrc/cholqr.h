@@ -39,9 +39,18 @@ struct SmallMmBatch {
 };
 int small_mm_batch(const SmallMmBatch& batch, int count, cudaStream_t stream);
 
-// P[0:b,0:b] <- diag(s) R on/above the diagonal, L1 below; tau_k = T_kk.
+// P[0:b,0:b] <- diag(s) R on/above the diagonal, L1 below; tau_k = T_kk; Tout <- T
+// (ld ldto) -- only when *flag == 0; otherwise the launch counts one fallback
+// panel on the device (cholqr_fallback_count) and writes nothing.
 int cholqr_write_top(double* P, int64_t ldp, int b, const double* R, const double* s,
                      const double* L1, const double* T, int64_t ldt, double* tau, int ldo,
-                     cudaStream_t stream);
+                     double* Tout, int64_t ldto, const int* flag, cudaStream_t stream);
+
+// inside a stream capture: sets the graph conditional h to (*flag != 0)
+int set_conditional_from_flag(cudaGraphConditionalHandle h, const int* flag, cudaStream_t stream);
+
+// panels (on the current device) whose CholeskyQR2 route fell back to the
+// Householder kernels; reads a device counter (synchronous)
+int64_t cholqr_fallback_count();
 
 }  // namespace qrb

@@ -174,6 +174,29 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// launch predicate: a kernel launched under a PredScope reads one device int at
+// entry and returns at once unless (*flag != 0) == want.  The CholeskyQR2 panel
+// uses it to choose its Householder fallback on the device, so the panel chain
+// never waits on a device->host flag read (and can be captured in a graph).
+// ---------------------------------------------------------------------------
+struct LaunchPred {
+  const int* flag;
+  int want;
+};
+__device__ __forceinline__ bool pred_off(const LaunchPred& p) {
+  if (p.flag == nullptr) return false;
+  const int v = *reinterpret_cast<const volatile int*>(p.flag);
+  return (v != 0) != (p.want != 0);
+}
+LaunchPred launch_pred();  // this host thread's current predicate ({nullptr, 0}: none)
+void set_launch_pred(LaunchPred p);
+struct PredScope {
+  LaunchPred old;
+  PredScope(const int* flag, int want) : old(launch_pred()) { set_launch_pred({flag, want}); }
+  ~PredScope() { set_launch_pred(old); }
+};
+
 // grid-wide barrier for cooperatively launched kernels. `counter` is zeroed
 // before the launch; `target` = (#barriers passed so far + 1) * gridDim.x.
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {

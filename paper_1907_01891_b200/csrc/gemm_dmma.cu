@@ -52,6 +52,7 @@ struct GemmArgs {
   int64_t split_stride;
   int mask_a, mask_b;
   int group_m;
+  LaunchPred pred;
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
@@ -123,6 +124,7 @@ template <bool A_KMAJOR, int BN, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_dmma_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, const GemmArgs args) {
+  if (pred_off(args.pred)) return;
   constexpr int NT = BN / 16;
   constexpr uint32_t A_BYTES = BM * BK * 8;
   constexpr uint32_t B_BYTES = BN * BK * 8;
@@ -335,6 +337,7 @@ struct NnArgs {
   int group_m;
   int num_tiles;
   int* counter;  // dynamic tile scheduler (async-epilogue kernel); nullptr = static
+  LaunchPred pred;
 };
 
 __device__ __forceinline__ double neg_bits(double x) {
@@ -355,6 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_nn_sub_persistent(const __grid_constant__ CUtensorMap mapA,
                            const __grid_constant__ CUtensorMap mapB,
                            const __grid_constant__ CUtensorMap mapC, const NnArgs args) {
+  if (pred_off(args.pred)) return;
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
   // keep the pointer derived from the __shared__ array so loads compile to LDS
@@ -497,6 +501,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_nn_sub_redadd(const __grid_constant__ CUtensorMap mapA,
                        const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
                        const int64_t ldc, const NnArgs args) {
+  if (pred_off(args.pred)) return;
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -632,6 +637,7 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
     gemm_nn_sub_asyncepi(const __grid_constant__ CUtensorMap mapA,
                          const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
                          const int64_t ldc, const NnArgs args) {
+  if (pred_off(args.pred)) return;
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -796,6 +802,7 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
     gemm_nn_sub_asyncepi_dyn(const __grid_constant__ CUtensorMap mapA,
                          const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
                          const int64_t ldc, const NnArgs args) {
+  if (pred_off(args.pred)) return;
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1047,6 +1054,7 @@ int launch(const MatView& a, const MatView& b, double* out, int64_t ldo, int64_t
   args.mask_a = mask_a;
   args.mask_b = mask_b;
   args.group_m = 16;
+  args.pred = launch_pred();
   const int num_m = (M + BM - 1) / BM;
   const int num_n = (N + BN - 1) / BN;
   const int nsplit = (K + kps - 1) / kps;
@@ -1063,6 +1071,9 @@ int launch(const MatView& a, const MatView& b, double* out, int64_t ldo, int64_t
 }  // namespace
 
 static thread_local int t_grid_cap = 0;
+static thread_local LaunchPred t_pred = {nullptr, 0};
+LaunchPred launch_pred() { return t_pred; }
+void set_launch_pred(LaunchPred p) { t_pred = p; }
 void gemm_set_grid_cap(int cap) { t_grid_cap = cap; }
 int gemm_grid_cap() { return t_grid_cap; }
 
@@ -1082,6 +1093,11 @@ int gemm_sm_count() {
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
   const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
   const int slots = gemm_sm_count();  // one 288-thread CTA per SM (168 regs)
+  // few output tiles (the panel's Gram matrices, late trailing updates): one
+  // wave whatever the split, so split as far as >= 128 rows of K per split
+  // allow (r02 trace: the 2160-row Gram ran 7 splits, 21 us)
+  if (tiles * 2 <= slots)
+    return std::max(1, std::min(std::min(max_splits, K / 128), slots / tiles));
   const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
   int best = 1;
   double best_eff = 0.0;
@@ -1145,6 +1161,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
     NnArgs args{};
+    args.pred = launch_pred();
     args.M = M;
     args.N = N;
     args.K = K;
@@ -1190,6 +1207,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     QRB_TRY(make_map(&ma, a_mm, 16, BK));
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
     NnArgs args{};
+    args.pred = launch_pred();
     args.M = M;
     args.N = N;
     args.K = K;
@@ -1210,6 +1228,7 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     QRB_TRY(make_map(&mb, b, BK, NN_BN));
     QRB_TRY(make_map(&mc, MatView{out, M, N, ldo}, 16, NN_BN));
     NnArgs args{};
+    args.pred = launch_pred();
     args.M = M;
     args.N = N;
     args.K = K;

@@ -45,6 +45,7 @@ struct PanelArgs {
   double* part;  // 2 x [(ib + 1) * P + ib] partial sums / pivot-row slots
   unsigned int* bar;
   unsigned long long* trace;  // optional per-phase timing (QRB_PANEL_TRACE)
+  LaunchPred pred;
 };
 
 // loads of data published by other CTAs before the last grid barrier; the
@@ -77,6 +78,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // column j+1 never overwrites partials another CTA is still summing.
 template <int OWN>  // columns owned per warp: ceil(ib / 16)
 __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p) {
+  if (pred_off(p.pred)) return;  // uniform over the grid: no CTA reaches a grid barrier
   extern __shared__ double smem_d[];
   const int R = p.R;
   const int ib = p.ib;
@@ -289,7 +291,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1) panel_qr_kernel(PanelArgs p)
 constexpr int BT_THREADS = 512;
 __global__ void __launch_bounds__(BT_THREADS) build_t_kernel(const double* G, int ldg,
                                                              const double* tau, int w, double* T,
-                                                             int ldt) {
+                                                             int ldt, const LaunchPred pred) {
+  if (pred_off(pred)) return;
   extern __shared__ double ts[];  // T: w*w column-major, then Z: w*32
   double* z = ts + (size_t)w * w;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -348,7 +351,9 @@ __global__ void __launch_bounds__(BT_THREADS) build_t_kernel(const double* G, in
 // from L2: latency-bound with few elements and many splits)
 template <int TPE>
 __global__ void reduce_splits_kernel(const double* parts, int64_t split_stride, int splits,
-                                     int rows, int cols, int64_t ldp, double* out, int64_t ldo) {
+                                     int rows, int cols, int64_t ldp, double* out, int64_t ldo,
+                                     const LaunchPred pred) {
+  if (pred_off(pred)) return;
   const int64_t total = (int64_t)rows * cols;
   const int sub = threadIdx.x % TPE, lane = threadIdx.x & 31;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / TPE;;
@@ -580,6 +585,7 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
   a.part = part;
   a.bar = bar;
   a.trace = nullptr;
+  a.pred = launch_pred();
   static unsigned long long* trace_buf = nullptr;
   static bool trace_on = std::getenv("QRB_PANEL_TRACE") != nullptr;
   if (trace_on) {
@@ -589,9 +595,26 @@ int panel_factor(const MatView& panel, int P, int R, double* tau, double* G, int
     }
     a.trace = trace_buf;
   }
+  // cooperative launch through cudaLaunchKernelEx (capturable into a graph).
+  // Under a launch predicate (the CholeskyQR2 fallback, normally skipped) the
+  // launch is NOT cooperative: a cooperative launch waits until all P CTAs fit
+  // at once, i.e. behind the look-ahead's capped update on the other SMs, even
+  // when every CTA would return at entry (r02: config-2 panel chain 69 -> 123
+  // ms).  P <= one CTA per SM and nothing waits on the panel while it runs, so
+  // CTAs of a taken fallback that start late only delay the barrier.
+  const bool coop = a.pred.flag == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P);
+  cfg.blockDim = dim3(PANEL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = coop ? 1 : 0;
   void* args[] = {&a};
-  QRB_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P),
-                                           dim3(PANEL_THREADS), args, smem, stream));
+  QRB_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
   if (trace_on) {
     static int calls = 0;
     static double cols_total = 0;
@@ -616,7 +639,7 @@ int build_t(const double* G, int ldg, const double* tau, int w, double* T, int l
             cudaStream_t stream) {
   const size_t smem = ((size_t)w * w + (size_t)w * 32) * sizeof(double);
   QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(build_t_kernel), smem));
-  build_t_kernel<<<1, BT_THREADS, smem, stream>>>(G, ldg, tau, w, T, ldt);
+  build_t_kernel<<<1, BT_THREADS, smem, stream>>>(G, ldg, tau, w, T, ldt, launch_pred());
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;
 }
@@ -632,19 +655,19 @@ int reduce_splits(const double* parts, int64_t split_stride, int splits, int row
   switch (tpe) {
     case 1:
       reduce_splits_kernel<1><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
-                                                          ldp, out, ldo);
+                                                          ldp, out, ldo, launch_pred());
       break;
     case 2:
       reduce_splits_kernel<2><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
-                                                          ldp, out, ldo);
+                                                          ldp, out, ldo, launch_pred());
       break;
     case 4:
       reduce_splits_kernel<4><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
-                                                          ldp, out, ldo);
+                                                          ldp, out, ldo, launch_pred());
       break;
     default:
       reduce_splits_kernel<8><<<blocks, 128, 0, stream>>>(parts, split_stride, splits, rows, cols,
-                                                          ldp, out, ldo);
+                                                          ldp, out, ldo, launch_pred());
   }
   QRB_CUDA_TRY(cudaGetLastError());
   return QRB_OK;

@@ -50,11 +50,22 @@ int set_max_dynamic_smem(const void* func, size_t bytes) {
 // ---------------------------------------------------------------------------
 // grow-only device buffers
 // ---------------------------------------------------------------------------
+// bumped whenever a device buffer is (re)allocated or a tuning knob changes: a
+// captured factorization graph (qrb_factorize) is valid only for the epoch it
+// was captured in
+static std::atomic<uint64_t> g_graph_epoch{1};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t need, cudaStream_t st) {
     if (need <= bytes) return QRB_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      set_last_error("device buffer growth during graph capture");
+      return QRB_ERR_STATE;  // the caller abandons the capture and runs eagerly
+    }
+    ++g_graph_epoch;
     if (p) {
       QRB_CUDA_TRY(cudaStreamSynchronize(st));
       QRB_CUDA_TRY(cudaFree(p));
@@ -83,13 +94,10 @@ struct Workspace {
   DevBuf Wq, small, flag;  // CholeskyQR2 panel: Q1 (m x b), 12 b x b blocks, status word
   DevBuf T2;               // merged block reflector of a panel pair (2nb x 2nb) + scratch
   DevBuf T4;               // scratch of the 4-panel merge (outer_panels = 4)
-  int* hflag = nullptr;    // pinned host copy of the status word
   int64_t w2_cols = 0;     // columns / width of the W2 the last apply_qt_w2 formed
   int64_t w2_w = 0;
   uint64_t w2_gen = 0;     // bumped by every apply_qt_w2 (qrb_op_apply_qt_cols checks it)
   void release() {
-    if (hflag) cudaFreeHost(hflag);
-    hflag = nullptr;
     Wq.release();
     small.release();
     T2.release();
@@ -344,15 +352,33 @@ static int g_panel_algo = [] {
   return e ? std::atoi(e) : 0;
 }();
 static int64_t g_cholqr_min_rows = 1024;  // CholeskyQR2 wins from ~2k rows up (r01 sweep)
-static std::atomic<int64_t> g_cholqr_panels{0}, g_cholqr_fallbacks{0};
+static std::atomic<int64_t> g_cholqr_panels{0};
+
+// a non-blocking stream per device for capturing conditional-node bodies
+static cudaStream_t capture_helper_stream() {
+  static cudaStream_t hs[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!hs[dev & 63] && cudaStreamCreateWithFlags(&hs[dev & 63], cudaStreamNonBlocking) != cudaSuccess)
+    hs[dev & 63] = nullptr;
+  return hs[dev & 63];
+}
+
+// Householder QR of the panel column by column (the path for short panels and
+// the CholeskyQR2 route's fallback)
+static int factor_panel_householder(const MatView& panel, double* tau, double* T, int64_t ldt,
+                                    Workspace& ws, cudaStream_t st);
 
 // CholeskyQR2 + Householder reconstruction of an m x b panel (cholqr.cu header
-// for the algebra).  Returns QRB_OK with *done = false, the panel untouched,
-// when the Cholesky route is not trustworthy for this panel (caller falls
-// back to the column-by-column Householder kernel).
+// for the algebra).  The small factorizations raise bits in a device flag when
+// the Cholesky route is not trustworthy for this panel; the completion kernels
+// run only when the flag is clear and the Householder kernels (launched right
+// after, predicated on the same flag) only when it is set -- the choice is made
+// on the device, so the panel chain never stops for a device->host flag read.
 static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, int64_t ldt,
-                                Workspace& ws, cudaStream_t st, bool* done) {
-  *done = false;
+                                Workspace& ws, cudaStream_t st) {
   const int m = static_cast<int>(panel.rows);
   const int b = static_cast<int>(panel.cols);
   const int64_t mw = (static_cast<int64_t>(m) + 1) & ~int64_t(1);
@@ -362,7 +388,6 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
   QRB_TRY(ws.small.ensure(sizeof(double) * (BLK * 13 + LD), st));
   QRB_TRY(ws.flag.ensure(64, st));
   QRB_TRY(ws.G.ensure(sizeof(double) * LD * 128, st));
-  if (!ws.hflag) QRB_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ws.hflag), 64));
   double* sb = ws.small.d();
   double *R1 = sb, *R1i = sb + BLK, *R2 = sb + 2 * BLK, *R2i = sb + 3 * BLK, *Qt = sb + 4 * BLK;
   double *Uc = sb + 5 * BLK, *NUcS = sb + 6 * BLK, *L1 = sb + 7 * BLK, *Uci = sb + 8 * BLK;
@@ -410,23 +435,66 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
     QRB_TRY(small_mm_batch(bt, 2, st));
   }
   g_launches += 8;
-  QRB_CUDA_TRY(cudaMemcpyAsync(ws.hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  QRB_CUDA_TRY(cudaStreamSynchronize(st));
   ++g_cholqr_panels;
-  if (*ws.hflag != 0) {
-    ++g_cholqr_fallbacks;
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  cudaGraph_t cg = nullptr;
+  QRB_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, nullptr, nullptr));
+  auto finish = [&](cudaStream_t s2) -> int {
+    // V below the top block: L2 = Q1[b:] R2^-1 Uc^-1 = Q1[b:] M, written over P[b:]
+    if (m > b)
+      QRB_TRY(gemm_nn(MatView{Wq + b, m - b, b, mw}, MatView{M, b, b, LD}, panel.ptr + b,
+                      panel.ld, m - b, b, b, GEMM_EPI_STORE, 0, s2));
+    QRB_TRY(cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, T, ldt, flag, s2));
+    g_launches += 2;
+    return QRB_OK;
+  };
+  if (cst == cudaStreamCaptureStatusActive) {
+    // captured (qrb_factorize graph): an IF/ELSE node on the flag -- the
+    // branch not taken costs nothing at replay
+    cudaGraphConditionalHandle hc;
+    QRB_CUDA_TRY(cudaGraphConditionalHandleCreate(&hc, cg, 0, 0));
+    QRB_TRY(set_conditional_from_flag(hc, flag, st));
+    g_launches += 1;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    QRB_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hc;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 2;
+    cudaGraphNode_t node;
+    QRB_CUDA_TRY(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
+    QRB_CUDA_TRY(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaStream_t hs = capture_helper_stream();
+    if (!hs) {
+      set_last_error("no capture helper stream");
+      return QRB_ERR_STATE;
+    }
+    for (int br = 0; br < 2; ++br) {
+      QRB_CUDA_TRY(cudaStreamBeginCaptureToGraph(hs, cp.conditional.phGraph_out[br], nullptr,
+                                                 nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      int rc = QRB_OK;
+      if (br == 0) {  // flag set: count the fallback, then the Householder kernels
+        rc = cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, T, ldt, flag, hs);
+        if (rc == QRB_OK) rc = factor_panel_householder(panel, tau, T, ldt, ws, hs);
+      } else {
+        rc = finish(hs);
+      }
+      cudaGraph_t body = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(hs, &body);
+      QRB_TRY(rc);
+      QRB_CUDA_TRY(ce);
+    }
     return QRB_OK;
   }
-  // V below the top block: L2 = Q1[b:] R2^-1 Uc^-1 = Q1[b:] M, written over P[b:]
-  if (m > b)
-    QRB_TRY(gemm_nn(MatView{Wq + b, m - b, b, mw}, MatView{M, b, b, LD}, panel.ptr + b, panel.ld,
-                    m - b, b, b, GEMM_EPI_STORE, 0, st));
-  QRB_TRY(cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, st));
-  QRB_CUDA_TRY(cudaMemcpy2DAsync(T, sizeof(double) * ldt, Tt, sizeof(double) * LD,
-                                 sizeof(double) * b, b, cudaMemcpyDeviceToDevice, st));
-  g_launches += 3;
-  *done = true;
-  return QRB_OK;
+  {
+    PredScope ok(flag, 0);
+    QRB_TRY(finish(st));
+  }
+  // fallback: the panel is still untouched when the flag is set
+  PredScope fb(flag, 1);
+  return factor_panel_householder(panel, tau, T, ldt, ws, st);
 }
 
 static bool cholqr_eligible(const MatView& panel) {
@@ -447,11 +515,14 @@ static int factor_panel_impl(const MatView& panel, double* tau, double* T, int64
     set_last_error("panel rows < width");
     return QRB_ERR_ARG;
   }
-  if (cholqr_eligible(panel)) {
-    bool done = false;
-    QRB_TRY(factor_panel_cholqr2(panel, tau, T, ldt, ws, st, &done));
-    if (done) return QRB_OK;
-  }
+  if (cholqr_eligible(panel)) return factor_panel_cholqr2(panel, tau, T, ldt, ws, st);
+  return factor_panel_householder(panel, tau, T, ldt, ws, st);
+}
+
+static int factor_panel_householder(const MatView& panel, double* tau, double* T, int64_t ldt,
+                                    Workspace& ws, cudaStream_t st) {
+  const int m = static_cast<int>(panel.rows);
+  const int pw = static_cast<int>(panel.cols);
   const int ldg = 128;
   QRB_TRY(ws.G.ensure(sizeof(double) * ldg * 128, st));
   QRB_TRY(ws.Ti.ensure(sizeof(double) * 128 * 128, st));
@@ -657,6 +728,14 @@ struct qrb_handle {
   cudaEvent_t ev_upd = nullptr, ev_pan = nullptr;
   DevBuf T2scratch;                           // merged reflectors of pairs not kept in T2
   DevBuf T4scratch;                           // merged 4nb x 4nb reflectors (outer_panels = 4)
+  // the whole right-looking factorization captured as one CUDA graph (small
+  // shapes, where the panel chain is launch-latency bound), replayed while the
+  // buffer / tuning epoch it was captured in holds
+  cudaGraphExec_t fgraph = nullptr;
+  uint64_t fgraph_epoch = 0;
+  int64_t fgraph_launches = 0;
+  std::vector<char> fgraph_t2;  // t2_valid as the captured run leaves it
+  bool fgraph_warm = false;     // one eager run first (sizes every buffer)
 };
 
 namespace {
@@ -697,9 +776,13 @@ struct ProfSession {
     if (!h->profiling) return;
     g_prof = nullptr;
     if (!rep) return;
+    static const bool dump = std::getenv("QRB_PROF_DUMP") != nullptr;
     for (auto& r : h->prof.recs) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, r.a, r.b);
+      if (dump)
+        std::fprintf(stderr, "[qrb prof] kind %d ms %.4f gflop %.3f tflops %.2f\n", r.kind, ms,
+                     r.flops * 1e-9, r.flops / (ms > 0 ? ms : 1e-9) * 1e-9);
       qrb_kernel_stat& k = rep->kernels[r.kind];
       k.ms += ms;
       k.flops += r.flops;
@@ -883,6 +966,12 @@ static std::atomic<int64_t> g_la_steps{0};
 // to 16384 / 32768 / 49152 remaining columns 34.75 / 34.75 / 34.63 TFLOP/s;
 // config 2 (16384 columns) never takes them)
 static int64_t g_outer4_min_cols = 24576;
+// factorizations with at most this many columns run as a captured CUDA graph
+// (qrb_set_tuning "graph_max_cols"; 0 = never)
+static int64_t g_graph_max_cols = [] {
+  const char* e = std::getenv("QRB_GRAPH_MAX_COLS");
+  return e ? std::atoll(e) : int64_t(16384);
+}();
 
 static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_t st) {
   const int nb = h->nb;
@@ -1017,6 +1106,75 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   return QRB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// graph-captured factorization (qrb_factorize, n <= graph_max_cols)
+//
+// Configs 1-2 are bound by the panel chain's launch latency (r02 trace of
+// config 1: 183 gaps, 0.6 of 3.3 ms idle).  With the CholeskyQR2 fallback
+// chosen on the device the whole right-looking schedule -- both streams of the
+// look-ahead included -- has no host decision left, so it is captured once per
+// handle and replayed as one graph.  The first factorization of a handle runs
+// eagerly (it sizes every buffer and creates the look-ahead stream); any buffer
+// growth or tuning change afterwards bumps g_graph_epoch and forces a fresh
+// capture.  A capture that fails for any reason runs the schedule eagerly.
+// Same kernels, same order, same shapes: the factors are bitwise those of the
+// eager run.
+// ---------------------------------------------------------------------------
+static std::atomic<int64_t> g_graph_captures{0}, g_graph_replays{0};
+
+static int factorize_graphed(qrb_handle* h, Workspace& ws, cudaStream_t st) {
+  const uint64_t epoch = g_graph_epoch.load();
+  if (h->fgraph && h->fgraph_epoch == epoch) {
+    ++g_graph_replays;
+    QRB_CUDA_TRY(cudaGraphLaunch(h->fgraph, st));
+    g_launches += h->fgraph_launches;
+    h->t2_valid = h->fgraph_t2;
+    return QRB_OK;
+  }
+  if (h->fgraph) {
+    cudaGraphExecDestroy(h->fgraph);
+    h->fgraph = nullptr;
+  }
+  if (!h->fgraph_warm) {
+    h->fgraph_warm = true;
+    return right_looking(h, 0, ws, st);
+  }
+  const int64_t l0 = g_launches.load();
+  if (!capture_helper_stream()) return right_looking(h, 0, ws, st);
+  QRB_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = right_looking(h, 0, ws, st);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  cudaGraphExec_t exec = nullptr;
+  bool ok = rc == QRB_OK && ce == cudaSuccess && graph != nullptr;
+  if (ok)
+    ok = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority) ==
+         cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {
+    static const bool dbg = std::getenv("QRB_GRAPH_DEBUG") != nullptr;
+    if (dbg)
+      std::fprintf(stderr, "[qrb] factorization capture failed: rc %d, %s, last error: %s\n", rc,
+                   cudaGetErrorString(ce), t_last_error.c_str());
+    cudaGetLastError();  // nothing ran during the capture: do it eagerly
+    g_launches = l0;
+    h->fgraph_epoch = 0;
+    return right_looking(h, 0, ws, st);
+  }
+  h->fgraph = exec;
+  h->fgraph_epoch = g_graph_epoch.load() == epoch ? epoch : 0;
+  h->fgraph_launches = g_launches.load() - l0;
+  h->fgraph_t2 = h->t2_valid;
+  ++g_graph_captures;
+  QRB_CUDA_TRY(cudaGraphLaunch(exec, st));
+  return QRB_OK;
+}
+
+static bool graph_eligible(const qrb_handle* h) {
+  return g_graph_max_cols > 0 && h->n <= g_graph_max_cols && !h->profiling && !g_prof &&
+         !gemm_nn_dynamic();
+}
+
 // what this host thread's last qrb_op_apply_qt_begin formed (checked by _cols)
 struct BeginRecord {
   uint64_t gen = 0;
@@ -1112,6 +1270,7 @@ int qrb_destroy(qrb_handle* h) {
   if (h->ev_pan) cudaEventDestroy(h->ev_pan);
   h->T2scratch.release();
   h->T4scratch.release();
+  if (h->fgraph) cudaGraphExecDestroy(h->fgraph);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return QRB_OK;
@@ -1203,7 +1362,10 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
   MatView A{h->A, h->m, h->n, h->lda};
   if (!timing) {
-    QRB_TRY(right_looking(h, 0, ws, st));
+    if (graph_eligible(h))
+      QRB_TRY(factorize_graphed(h, ws, st));
+    else
+      QRB_TRY(right_looking(h, 0, ws, st));
   } else {
     for (int k = 0; k < h->npanels; ++k) {  // serial, single panels, per-phase events
       const int64_t j0 = int64_t(k) * h->nb;
@@ -1778,6 +1940,11 @@ int64_t qrb_launch_count(void) { return g_launches.load(); }
 
 int qrb_set_tuning(const char* key, int64_t value) {
   const std::string k = key ? key : "";
+  ++g_graph_epoch;  // captured factorization graphs bake the knobs in
+  if (k == "graph_max_cols" && value >= 0) {
+    g_graph_max_cols = value;
+    return QRB_OK;
+  }
   if (k == "panel_algo" && value >= 0 && value <= 2) {
     g_panel_algo = static_cast<int>(value);
     return QRB_OK;
@@ -1846,7 +2013,10 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
   else if (k == "la_steps") *value = g_la_steps.load();
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
-  else if (k == "cholqr_fallbacks") *value = g_cholqr_fallbacks.load();
+  else if (k == "cholqr_fallbacks") *value = cholqr_fallback_count();
+  else if (k == "graph_max_cols") *value = g_graph_max_cols;
+  else if (k == "graph_captures") *value = g_graph_captures.load();
+  else if (k == "graph_replays") *value = g_graph_replays.load();
   else {
     set_last_error("qrb_get_tuning: unknown key: " + k);
     return QRB_ERR_ARG;
