@@ -179,9 +179,48 @@ def measure_config(cfg: int, reps: int = 3) -> dict:
            "slices": S, "qr_tflops": qr_flops(m, n) / (f_ms * 1e-3) / 1e12,
            "pct_fp64_peak": qr_flops(m, n) / (f_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
            "factor_ms": f_ms, "solve_ms": s_ms, "slices_per_s": S / (s_ms * 1e-3),
-           "timing": f"best of {reps} after a warm-up, device-resident A and B"}
+           "timing": f"best of {reps} after a warm-up, device-resident A and B",
+           "pair_chain": [pair_chain_ms(m), pair_chain_ms(m - n + 256)]}
     del a, b, x, xt
     torch.cuda.empty_cache()
+    return out
+
+
+def pair_chain_ms(m: int, nb: int = 128, reps: int = 5) -> dict:
+    """Latency of one panel-pair chain (factor panel a, Q_a^T on panel b, factor
+    panel b, merge T2: qrb_op_panel_block on an m x 2nb block), the chain the
+    look-ahead hides under the trailing update: on all SMs and with the GEMMs
+    capped to the look-ahead's share (qrb tuning la_sms).  Best of `reps`."""
+    import ctypes
+    import torch
+    from paper_1907_01891_b200 import _native as native
+    lib = native.load()
+    w = 2 * nb
+    ld = m + (m & 1)
+    g = torch.Generator(device="cuda").manual_seed(m)
+    a0 = torch.randn((w, ld), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.empty_like(a0)
+    tau = torch.zeros(w, dtype=torch.float64, device="cuda")
+    t = torch.zeros((2, nb, nb), dtype=torch.float64, device="cuda")
+    t2 = torch.zeros((w, w), dtype=torch.float64, device="cuda")
+    P = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+    out = {"m": m, "w": w}
+    la = native.get_tuning("la_sms")
+    for label, cap in (("all_sms_ms", 0), (f"{la}_sms_ms", la)):
+        native.set_tuning("grid_cap", cap)
+        best = 1e30
+        for it in range(reps + 1):
+            a.copy_(a0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            native.check(lib.qrb_op_panel_block(P(a), ld, m, w, nb, P(tau), P(t), P(t2), w, None, 0),
+                         "qrb_op_panel_block")
+            e1.record()
+            torch.cuda.synchronize()
+            if it:
+                best = min(best, e0.elapsed_time(e1))
+        out[label] = round(best, 4)
+    native.set_tuning("grid_cap", 0)
     return out
 
 
@@ -547,6 +586,7 @@ def ours_arm(args, rank: int, world: int):
                          "slices_per_s": cpu["slices_per_s"], "op_seconds": cpu["op_seconds"]},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "config5": cfg5, "other_configs": others or None, "quality": quality,
+        "pair_chain": [pair_chain_ms(m, args.nb), pair_chain_ms(m - n + 2 * args.nb, args.nb)],
         "check": {"resid_identity_max_rel": resid_rel, "resid_sample": resid_dbg},
         "setup_s": setup_s, "densify_s": densify_s,
     }

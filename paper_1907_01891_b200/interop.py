@@ -126,3 +126,49 @@ def solve_reference_factors(f: ReferenceFactors, bmat: np.ndarray):
         y[:, k * b + extent:(k + 1) * b] = 0.0
     torch.cuda.synchronize()
     return y[:, :f.cols].cpu().numpy().T.copy()
+
+
+def export_reference_factors(directory, factored: np.ndarray, t_blocks: np.ndarray, nb: int,
+                             geometry_hash: str = "") -> ReferenceFactors:
+    """Write a GPU factorization as an ``oocqr`` factors directory that the
+    reference's own ``solve`` reads (meta.txt, ``factored/``, ``s/``;
+    task_engine.py:531-594, storage conventions kernels.py:6-20).
+
+    The GPU factorization is one blocked Householder QR of the whole m x n
+    matrix with panel width nb: R on/above the diagonal, unit-lower reflectors
+    below it, one nb x nb T per panel, Q = H_0 H_1 ... with H_p = I - V_p T_p
+    V_p^T.  In the reference's format that is exactly a ONE-tile factorization
+    (tile size b = m rounded up to nb, grid 1 x 1, inner_block = nb): the
+    reference's ``comp_dense_qr`` of a single b x b tile is the same panel
+    recurrence and stores the same (R, V) in the tile and T_p packed at rows
+    p*nb : p*nb + nb, columns 0 : nb of the S tile.  Zero padding rows/columns
+    (tile_store.py:186-187) contribute nothing: padded reflector columns have
+    T = 0.  A multi-tile-row export is not possible without refactoring: the
+    reference's Q is a product of per-tile-pair (TD) reflectors, ours of
+    full-height panel reflectors.  The caller's right-hand sides must therefore
+    be tiled with the same tile size b (``solve`` checks it).
+
+    factored: m x n (host) as QrDevice.get_matrix() returns it; t_blocks:
+    nb x (npanels * nb) as QrDevice.factors()[1] returns it.
+    """
+    directory = Path(directory)
+    factored = np.asarray(factored, dtype=np.float64)
+    m, n = factored.shape
+    npan = -(-n // nb)
+    if t_blocks.shape != (nb, npan * nb):
+        raise ValueError(f"T blocks must be {nb} x {npan * nb}, got {t_blocks.shape}")
+    b = -(-m // nb) * nb
+    directory.mkdir(parents=True, exist_ok=True)
+    fac = TiledMatrix.create(m, n, b, directory / "factored")
+    s_store = TiledMatrix.create(b, b, b, directory / "s")
+    tile = np.zeros((b, b))
+    tile[:m, :n] = factored
+    fac.store_tile(TileId(0, 0), tile)
+    tile[:] = 0.0
+    for p in range(npan):
+        w = min(nb, n - p * nb)
+        tile[p * nb:p * nb + w, :w] = np.triu(t_blocks[:w, p * nb:p * nb + w])
+    s_store.store_tile(TileId(0, 0), tile)
+    f = ReferenceFactors(fac, s_store, m, n, b, nb, geometry_hash)
+    f.save(directory)
+    return f

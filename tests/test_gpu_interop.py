@@ -52,3 +52,49 @@ def test_reference_factors_singular_order(tmp_path, golden):
     with pytest.raises(pkg.SingularMatrixError) as e:
         solve_reference_factors(rf, z["c3_19_b"])
     assert e.value.global_column == int(z["c3_19_col"][0])
+
+
+def _materialise(z, prefix, directory):
+    """Write the oocqr-written factors directory stored byte for byte in the
+    fixture (tests/golden/make_golden_factors.py) back to disk."""
+    for i, rel in enumerate(z[f"{prefix}_paths"]):
+        p = directory / str(rel)
+        p.parent.mkdir(parents=True, exist_ok=True)
+        p.write_bytes(z[f"{prefix}_file{i}"].tobytes())
+
+
+@pytest.mark.parametrize("tile", [128, 256])
+def test_solve_with_oocqr_written_factors(tmp_path, golden, tile):
+    """Factors written by the reference's own factorize() (not the oracle):
+    the GPU replay of its solve task order gives the reference's own X."""
+    from paper_1907_01891_b200.interop import ReferenceFactors, solve_reference_factors
+    z = golden("ref_factors_ct0.npz")
+    _materialise(z, f"t{tile}", tmp_path)
+    rf = ReferenceFactors.load(tmp_path)
+    assert (rf.tile_size, rf.inner_block) == tuple(int(v) for v in z[f"t{tile}_tiling"])
+    x = solve_reference_factors(rf, z["b"])
+    assert rel_err(x, z[f"t{tile}_x"]) <= 1e-10
+
+
+def test_export_roundtrip_through_reference_format(tmp_path):
+    """GPU factors exported in the reference's layout (one tile, inner block =
+    panel width) and replayed with the reference's solve task order give the
+    GPU's own solution."""
+    from paper_1907_01891_b200 import ct_system as cs
+    from paper_1907_01891_b200.device import QrDevice
+    from paper_1907_01891_b200.interop import (ReferenceFactors, export_reference_factors,
+                                               solve_reference_factors)
+    g = cs.config_geometry(1)
+    a = cs.dense_matrix(g)
+    b = cs.noisy_sinograms(a @ cs.phantom_stack(1, 3), 1)
+    with QrDevice(*a.shape) as q:
+        q.set_matrix(a)
+        q.factorize()
+        fac = q.get_matrix()
+        _, t = q.factors()
+        x_gpu, _, _ = q.solve(b)
+    export_reference_factors(tmp_path, fac, t, 128, cs.geometry_hash(g))
+    rf = ReferenceFactors.load(tmp_path)
+    assert rf.tile_size >= a.shape[0] and rf.factored.grid_rows == 1
+    x = solve_reference_factors(rf, b)
+    assert rel_err(x, x_gpu) <= 1e-10
