@@ -99,6 +99,14 @@ QRB_API int qrb_set_device(int device);
  * (reference EngineConfig.inner_block, task_engine.py:77-121).
  * Replaces: factorize's store setup (task_engine.py:614-628). */
 QRB_API int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out);
+
+/* As qrb_create, but over the caller's device matrix A (column-major, ld even
+ * and >= m, 16-byte aligned), factored in place; A is not freed by
+ * qrb_destroy.  The in-core step of the host-staged (out-of-HBM) engine
+ * (ooc.py; replaces the reference's in-cache execution of a tile column's
+ * tasks, task_engine.py:330-474). */
+QRB_API int qrb_create_view(int device, int64_t m, int64_t n, int nb, double* A, int64_t lda,
+                            qrb_handle** out);
 QRB_API int qrb_destroy(qrb_handle* h);
 
 /* Copy columns [col0, col0+ncols) of A in/out (column-major, leading dim ld).
@@ -141,6 +149,13 @@ QRB_API int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int
  * (nb x nb each, panel k at T + k*nb*ldt... stored as an nb x (npanels*nb) matrix). */
 QRB_API int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt);
 QRB_API int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t ldt);
+
+/* Merged 2nb x 2nb block reflectors of the panel pairs (2p, 2p+1) of a factored
+ * handle, pair p at columns [2nb p, 2nb (p+1)) of a 2nb x (npanels/2 * 2nb)
+ * matrix with leading dim ldt2 (zeros where a pair does not exist).  Host or
+ * device destination.  Lets later column blocks apply Q^T two panels at a
+ * time (K = 2nb GEMMs; kernels.py:324-341 applies one inner panel at a time). */
+QRB_API int qrb_get_pair_factors(qrb_handle* h, double* T2, int64_t ldt2);
 
 /* X = R^-1 (Q^T B)[0:n] for nrhs right-hand sides; resid[j] = ||(Q^T B)[n:m, j]||_2
  * (= ||A x_j - b_j||_2; may be NULL).  B is m x nrhs (ldb), X is n x nrhs (ldx).

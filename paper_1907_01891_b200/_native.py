@@ -70,6 +70,8 @@ SIGNATURES = {
     "qrb_device_count": (c_int, [ctypes.POINTER(c_int)]),
     "qrb_set_device": (c_int, [c_int]),
     "qrb_create": (c_int, [c_int, c_i64, c_i64, c_int, ctypes.POINTER(c_void_p)]),
+    "qrb_create_view": (c_int, [c_int, c_i64, c_i64, c_int, c_void_p, c_i64,
+                                ctypes.POINTER(c_void_p)]),
     "qrb_destroy": (c_int, [c_void_p]),
     "qrb_set_matrix": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_int]),
     "qrb_get_matrix": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_int]),
@@ -78,6 +80,7 @@ SIGNATURES = {
     "qrb_factorize": (c_int, [c_void_p, ctypes.POINTER(QrbReport)]),
     "qrb_factorize_host": (c_int, [c_void_p, c_void_p, c_i64, c_i64, ctypes.POINTER(QrbReport)]),
     "qrb_get_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
+    "qrb_get_pair_factors": (c_int, [c_void_p, c_void_p, c_i64]),
     "qrb_set_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_solve": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p, c_int,
                           c_i64, ctypes.POINTER(QrbReport)]),

@@ -710,6 +710,7 @@ struct qrb_handle {
   double* T = nullptr;     // nb x (npanels * nb), ld = nb
   double* Rinv = nullptr;  // npanels blocks of nb x nb
   bool factored = false;
+  bool owns_a = true;      // false for qrb_create_view (A is the caller's memory)
   bool rinv_ready = false;
   double* T2 = nullptr;    // merged 2nb x 2nb reflectors of panel pairs (kept from the
   bool t2_ready = false;   //   factorization's pair steps, the rest filled at the first solve)
@@ -1201,7 +1202,8 @@ int qrb_set_device(int device) {
   return QRB_OK;
 }
 
-int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
+static int create_handle(int device, int64_t m, int64_t n, int nb, double* view, int64_t ld,
+                         qrb_handle** out) {
   if (!out || m < 1 || n < 1 || m < n || nb < 16 || nb > 128 || (nb % 16) != 0) {
     set_last_error("qrb_create: need m >= n >= 1 and nb in {16, 32, ..., 128}");
     return QRB_EARG;
@@ -1210,21 +1212,29 @@ int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
     set_last_error("qrb_create: dimensions exceed int32 TMA coordinates");
     return QRB_EARG;
   }
+  if (view && (ld < m || (ld & 1) || (reinterpret_cast<uintptr_t>(view) & 15))) {
+    set_last_error("qrb_create_view: need ld >= m, ld even and a 16-byte aligned matrix");
+    return QRB_EARG;
+  }
   *out = nullptr;
   QRB_CUDA_TRY(cudaSetDevice(device));
   qrb_handle* h = new qrb_handle();
   h->device = device;
   h->m = m;
   h->n = n;
-  h->lda = (m + 31) & ~int64_t(31);
+  h->lda = view ? ld : (m + 31) & ~int64_t(31);
   h->nb = nb;
   h->npanels = static_cast<int>((n + nb - 1) / nb);
+  h->owns_a = view == nullptr;
   auto fail = [&](const char* what) {
     set_last_error(std::string("qrb_create: ") + what);
     qrb_destroy(h);
     return QRB_ENOMEM;
   };
-  if (cudaMalloc(&h->A, sizeof(double) * h->lda * n) != cudaSuccess) return fail("matrix alloc");
+  if (view)
+    h->A = view;
+  else if (cudaMalloc(&h->A, sizeof(double) * h->lda * n) != cudaSuccess)
+    return fail("matrix alloc");
   if (cudaMalloc(&h->tau, sizeof(double) * n) != cudaSuccess) return fail("tau alloc");
   if (cudaMalloc(&h->T, sizeof(double) * nb * nb * h->npanels) != cudaSuccess)
     return fail("T alloc");
@@ -1238,11 +1248,24 @@ int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
   QRB_CUDA_TRY(cudaEventCreate(&h->ev0));
   QRB_CUDA_TRY(cudaEventCreate(&h->ev1));
   QRB_CUDA_TRY(cudaEventCreate(&h->ev2));
-  QRB_CUDA_TRY(cudaMemsetAsync(h->A, 0, sizeof(double) * h->lda * n, h->stream));
+  if (!view) QRB_CUDA_TRY(cudaMemsetAsync(h->A, 0, sizeof(double) * h->lda * n, h->stream));
   QRB_CUDA_TRY(cudaMemsetAsync(h->T, 0, sizeof(double) * nb * nb * h->npanels, h->stream));
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   *out = h;
   return QRB_OK;
+}
+
+int qrb_create(int device, int64_t m, int64_t n, int nb, qrb_handle** out) {
+  return create_handle(device, m, n, nb, nullptr, 0, out);
+}
+
+int qrb_create_view(int device, int64_t m, int64_t n, int nb, double* A, int64_t lda,
+                    qrb_handle** out) {
+  if (!A) {
+    set_last_error("qrb_create_view: null matrix");
+    return QRB_EARG;
+  }
+  return create_handle(device, m, n, nb, A, lda, out);
 }
 
 int qrb_destroy(qrb_handle* h) {
@@ -1250,7 +1273,7 @@ int qrb_destroy(qrb_handle* h) {
   DeviceGuard g(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->own_stream && h->own_stream != h->stream) cudaStreamSynchronize(h->own_stream);
-  if (h->A) cudaFree(h->A);
+  if (h->A && h->owns_a) cudaFree(h->A);
   if (h->tau) cudaFree(h->tau);
   if (h->T) cudaFree(h->T);
   if (h->Rinv) cudaFree(h->Rinv);
@@ -1578,12 +1601,39 @@ int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt) {
   if (!h || (T && ldt < h->nb)) return QRB_EARG;
   DeviceGuard g(h->device);
   if (tau)
-    QRB_CUDA_TRY(cudaMemcpyAsync(tau, h->tau, sizeof(double) * h->n, cudaMemcpyDeviceToHost,
+    QRB_CUDA_TRY(cudaMemcpyAsync(tau, h->tau, sizeof(double) * h->n, cudaMemcpyDefault,
                                  h->stream));
   if (T)
     QRB_CUDA_TRY(cudaMemcpy2DAsync(T, ldt * sizeof(double), h->T, h->nb * sizeof(double),
                                    h->nb * sizeof(double), int64_t(h->npanels) * h->nb,
-                                   cudaMemcpyDeviceToHost, h->stream));
+                                   cudaMemcpyDefault, h->stream));
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return QRB_OK;
+}
+
+int qrb_get_pair_factors(qrb_handle* h, double* T2, int64_t ldt2) {
+  const int64_t w2 = 2 * int64_t(h ? h->nb : 0);
+  if (!h || !T2 || ldt2 < w2) {
+    set_last_error("qrb_get_pair_factors: bad arguments");
+    return QRB_EARG;
+  }
+  if (!h->factored) {
+    set_last_error("qrb_get_pair_factors: handle is not factored");
+    return QRB_ESTATE;
+  }
+  DeviceGuard g(h->device);
+  QRB_TRY(ensure_t2(h, device_workspace()));
+  const int npairs = h->npanels / 2;
+  for (int p = 0; p < npairs; ++p) {
+    double* dst = T2 + int64_t(p) * w2 * ldt2;
+    if (pair_ok(h, 2 * p))
+      QRB_CUDA_TRY(cudaMemcpy2DAsync(dst, ldt2 * sizeof(double), h->T2 + p * w2 * w2,
+                                     w2 * sizeof(double), w2 * sizeof(double), w2,
+                                     cudaMemcpyDefault, h->stream));
+    else
+      QRB_CUDA_TRY(cudaMemset2DAsync(dst, ldt2 * sizeof(double), 0, w2 * sizeof(double), w2,
+                                     h->stream));
+  }
   QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return QRB_OK;
 }

@@ -95,6 +95,10 @@ CONFIGS = {
     # 720/512 -> 90/64, 375/512 -> 47/64; m/n = 1.03 as at full size): the
     # reduced instance the reference can factor here
     6: dict(image=64, views=90, bins=47, slices=8),
+    # the same family at ~1/1.41 the width (362 x 362 image, 509 views x 265 bins:
+    # A = 134885 x 131044, 141 GB -- half of config 4's rows and columns): the
+    # host-staged (out-of-HBM) engine's hardware run (profiles/r02_ooc_*)
+    7: dict(image=362, views=509, bins=265, slices=16),
 }
 
 

@@ -38,6 +38,7 @@ import numpy as np
 
 from . import _native
 from .errors import SingularMatrixError
+from .ooc import _StagedFactors
 from .tile_store import TiledMatrix
 
 
@@ -45,7 +46,7 @@ def _p(t, off: int = 0) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr() + 8 * off)
 
 
-class DiskStagedQR:
+class DiskStagedQR(_StagedFactors):
     """QR of the tiled matrix ``src`` (m x n on disk) into the tiled store
     ``dst`` (R on/above the diagonal, unit-lower reflectors below, the
     reference's factored layout), using at most ``budget_bytes`` of HBM for the
@@ -65,24 +66,20 @@ class DiskStagedQR:
         self.m, self.n, self.nb = m, n, nb
         self.lda = (m + 31) // 32 * 32
         self.npan = -(-n // nb)
-        col_bytes = 8 * self.lda
-        stage = 2 * col_bytes * nb
-        sp_panels = max(1, (int(budget_bytes) - stage) // (col_bytes * nb))
-        self.sp_cols = min(n, sp_panels * nb)
+        self.sp_cols = self.super_panel_cols(n, nb, self.lda, budget_bytes)
         dev = torch.device("cuda")
-        self.t_all = torch.zeros((self.npan * nb, nb), dtype=torch.float64, device=dev)
-        self.tau = torch.zeros(self.npan * nb, dtype=torch.float64, device=dev)
+        self._init_factors(dev)
         self.copy_stream = torch.cuda.Stream()
         self.pool = ThreadPoolExecutor(max_workers=max(1, io_threads))     # reads
         self.wpool = ThreadPoolExecutor(max_workers=max(1, io_threads))    # write-back
-        self.hbuf = [torch.empty((nb, self.lda), dtype=torch.float64, pin_memory=True)
+        self.hbuf = [torch.empty((2 * nb, self.lda), dtype=torch.float64, pin_memory=True)
                      for _ in range(2)]
         # write-back ring: bounded pinned memory, a slot is reused once its write is done
         self.wbuf = [torch.empty((nb, self.lda), dtype=torch.float64, pin_memory=True)
                      for _ in range(3)]
         self.wfut: list = [None] * len(self.wbuf)
         self._wslot = 0
-        self.dbuf = [torch.empty((nb, self.lda), dtype=torch.float64, device=dev)
+        self.dbuf = [torch.empty((2 * nb, self.lda), dtype=torch.float64, device=dev)
                      for _ in range(2)]
         self.stats: dict = {}
         self._io = {"read_bytes": 0, "write_bytes": 0, "read_s": 0.0, "write_s": 0.0}
@@ -92,12 +89,13 @@ class DiskStagedQR:
         self.wpool.shutdown(wait=True)
 
     # -- I/O -------------------------------------------------------------------------
-    def _read(self, store: TiledMatrix, k: int, row0: int, row1: int | None, hb, wait_evt):
-        """Worker: panel k rows [row0, row1) of ``store`` into the pinned buffer hb."""
+    def _read(self, store: TiledMatrix, k: int, row0: int, row1: int | None, w: int, hb,
+              wait_evt):
+        """Worker: columns [k nb, k nb + w) rows [row0, row1) of ``store`` into
+        the pinned buffer hb."""
         if wait_evt is not None:
             wait_evt.synchronize()          # the previous H2D out of hb has finished
         c0 = k * self.nb
-        w = min(self.nb, self.n - c0)
         t0 = time.perf_counter()
         view = hb.numpy().T                 # (lda, nb) Fortran
         store.read_columns(c0, w, row0, view, row1)
@@ -107,8 +105,8 @@ class DiskStagedQR:
 
     def _stream(self, store: TiledMatrix, items, consume) -> None:
         """Double-buffered disk -> pinned -> HBM pipeline over ``items`` =
-        [(k, row0, row1)], calling consume(k, device_buffer) on the current
-        stream for each, in order."""
+        [(k, row0, row1, width)] (columns [k nb, k nb + width)), calling
+        consume(item, device_buffer) on the current stream for each, in order."""
         import torch
 
         cur = torch.cuda.current_stream()
@@ -120,24 +118,25 @@ class DiskStagedQR:
         def submit(idx):
             if idx < len(items):
                 s = idx % 2
-                k, r0, r1 = items[idx]
-                futs[idx] = self.pool.submit(self._read, store, k, r0, r1, self.hbuf[s],
+                k, r0, r1, w = items[idx][:4]
+                futs[idx] = self.pool.submit(self._read, store, k, r0, r1, w, self.hbuf[s],
                                              h2d[s] if h2d_recorded[s] else None)
 
         submit(0)
         submit(1)
-        for idx, (k, r0, r1) in enumerate(items):
+        for idx, item in enumerate(items):
+            k, r0, r1, w = item[:4]
             s = idx % 2
             futs.pop(idx).result()
             r1 = self.m if r1 is None else r1
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(used[s])
-                self.dbuf[s][:, r0:r1].copy_(self.hbuf[s][:, r0:r1], non_blocking=True)
+                self.dbuf[s][:w, r0:r1].copy_(self.hbuf[s][:w, r0:r1], non_blocking=True)
                 h2d[s].record(self.copy_stream)
                 h2d_recorded[s] = True
             submit(idx + 2)                 # waits on h2d[s] before refilling hbuf[s]
             cur.wait_event(h2d[s])
-            consume(k, self.dbuf[s])
+            consume(item, self.dbuf[s])
             used[s].record(cur)
 
     def _write_superpanel(self, d, c0: int, c1: int) -> list:
@@ -187,36 +186,25 @@ class DiskStagedQR:
             w = c1 - c0
             d[:w].zero_()
 
-            def load(k, buf, c0=c0):
-                kw = min(nb, n - k * nb)
+            def load(item, buf, c0=c0):
+                k, kw = item[0], item[3]
                 d[k * nb - c0:k * nb - c0 + kw, :m].copy_(buf[:kw, :m])
 
-            self._stream(self.src, [(k, 0, None) for k in range(c0 // nb, -(-c1 // nb))], load)
+            self._stream(self.src, [(k, 0, None, min(nb, n - k * nb))
+                                    for k in range(c0 // nb, -(-c1 // nb))], load)
             # reflectors of earlier super-panels must be on disk before they are streamed
             for f in pending:
                 f.result()
             pending = []
 
-            def apply(k, buf, c0=c0, w=w):
-                j0 = k * nb
-                pw = min(nb, n - j0)
-                chk(self.lib.qrb_op_apply_qt(_p(buf, j0), lda, m - j0, pw,
-                                             _p(self.t_all, k * nb * nb), nb,
-                                             _p(d, j0), lda, w, None), "qrb_op_apply_qt")
+            def apply(item, buf, w=w):
+                k, np_ = item[0], item[4]
+                self._apply_block(k, np_, buf, k * nb, d, k * nb, w)
 
-            self._stream(self.dst, [(k, k * nb, None) for k in range(c0 // nb)], apply)
-            for k in range(c0 // nb, -(-c1 // nb)):
-                j0 = k * nb
-                pw = min(nb, n - j0)
-                lc = j0 - c0
-                chk(self.lib.qrb_op_panel(_p(d, j0 + lc * lda), lda, m - j0, pw, _p(self.tau, j0),
-                                          _p(self.t_all, k * nb * nb), nb, None), "qrb_op_panel")
-                rest = w - (lc + pw)
-                if rest > 0:
-                    chk(self.lib.qrb_op_apply_qt(_p(d, j0 + lc * lda), lda, m - j0, pw,
-                                                 _p(self.t_all, k * nb * nb), nb,
-                                                 _p(d, j0 + (lc + pw) * lda), lda, rest, None),
-                        "qrb_op_apply_qt")
+            self._stream(self.dst, [(k, k * nb, None, self._block_width(k, np_), np_)
+                                    for k, np_ in self._blocks(c0 // nb)], apply)
+            # right-looking inside the super-panel (the device driver)
+            self._factor_in_core(d, c0, w)
             pending = self._write_superpanel(d, c0, c1)
         for f in pending:
             f.result()
@@ -259,17 +247,16 @@ class DiskStagedQR:
         y = b_dev.clone()
         chk = _native.check
 
-        def apply(k, buf):
-            j0 = k * nb
-            pw = min(nb, n - j0)
-            chk(self.lib.qrb_op_apply_qt(_p(buf, j0), lda, m - j0, pw,
-                                         _p(self.t_all, k * nb * nb), nb, _p(y, j0), lda, s,
-                                         None), "qrb_op_apply_qt")
+        def apply(item, buf):
+            k, np_ = item[0], item[4]
+            self._apply_block(k, np_, buf, k * nb, y, k * nb, s)
 
-        self._stream(self.dst, [(k, k * nb, None) for k in range(self.npan)], apply)
+        self._stream(self.dst, [(k, k * nb, None, self._block_width(k, np_), np_)
+                                for k, np_ in self._blocks(self.npan)], apply)
         resid = torch.linalg.norm(y[:, n:m], dim=1)
 
-        def back(k, buf):
+        def back(item, buf):
+            k = item[0]
             i0 = k * nb
             bs = min(nb, n - i0)
             chk(self.lib.qrb_op_trsm_upper(_p(buf, i0), lda, bs, 16, _p(y, i0), lda, s, None),
@@ -278,7 +265,7 @@ class DiskStagedQR:
                 chk(self.lib.qrb_op_gemm_nn_sub(_p(buf), lda, _p(y, i0), lda, _p(y), lda, i0, s,
                                                 bs, None), "qrb_op_gemm_nn_sub")
 
-        self._stream(self.dst, [(k, 0, k * nb + min(nb, n - k * nb))
+        self._stream(self.dst, [(k, 0, k * nb + min(nb, n - k * nb), min(nb, n - k * nb))
                                 for k in range(self.npan - 1, -1, -1)], back)
         torch.cuda.synchronize()
         return y[:, :n], resid

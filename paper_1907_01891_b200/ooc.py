@@ -38,10 +38,98 @@ def _p(t, off: int = 0) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr() + 8 * off)
 
 
-class HostStagedQR:
+class _StagedFactors:
+    """State and steps shared by the host- and disk-staged engines: per-panel T
+    and tau, the merged pair reflectors, the in-core super-panel factorization
+    and the reflector block schedule of the left-looking stream.  Subclasses
+    set lib, m, n, nb, lda, npan, device, t_all, t2_all, pair_valid, tau."""
+
+    def _init_factors(self, dev) -> None:
+        import torch
+
+        nb, w2 = self.nb, 2 * self.nb
+        self.device = torch.cuda.current_device()
+        self.t_all = torch.zeros((self.npan * nb, nb), dtype=torch.float64, device=dev)
+        self.t2_all = torch.zeros((max(1, self.npan // 2) * w2, w2), dtype=torch.float64,
+                                  device=dev)
+        self.pair_valid = np.zeros(max(1, self.npan // 2), dtype=bool)
+        self.tau = torch.zeros(self.npan * nb, dtype=torch.float64, device=dev)
+
+    @staticmethod
+    def super_panel_cols(n: int, nb: int, lda: int, budget_bytes: int) -> int:
+        """Columns of a super-panel: a whole number of panel pairs that fits the
+        HBM budget next to two pair-wide reflector staging buffers."""
+        w2 = 2 * nb
+        col_bytes = 8 * lda
+        sp_pairs = max(1, (int(budget_bytes) - 2 * col_bytes * w2) // (col_bytes * w2))
+        return min(n, sp_pairs * w2)
+
+    def _blocks(self, upto: int):
+        """Reflector blocks of panels [0, upto): (first panel, panels) -- merged
+        pairs where the in-core step formed one, single panels otherwise."""
+        k = 0
+        while k < upto:
+            if k % 2 == 0 and k + 1 < upto and self.pair_valid[k // 2]:
+                yield k, 2
+                k += 2
+            else:
+                yield k, 1
+                k += 1
+
+    def _block_width(self, k: int, panels: int) -> int:
+        return min(panels * self.nb, self.n - k * self.nb)
+
+    def _apply_block(self, k: int, panels: int, v, v_row_off: int, c, c_row_off: int,
+                     ncols: int) -> None:
+        """C[rows k nb.., :ncols] <- Q_block^T C, V of the block in v (ld lda)."""
+        j0 = k * self.nb
+        w = self._block_width(k, panels)
+        if panels == 2:
+            t, ldt = _p(self.t2_all, (k // 2) * 4 * self.nb * self.nb), 2 * self.nb
+        else:
+            t, ldt = _p(self.t_all, k * self.nb * self.nb), self.nb
+        st = self.lib.qrb_op_apply_qt(_p(v, v_row_off), self.lda, self.m - j0, w, t, ldt,
+                                      _p(c, c_row_off), self.lda, ncols, None)
+        _native.check(st, "qrb_op_apply_qt")
+
+    def _factor_in_core(self, d, c0: int, w: int) -> None:
+        """Factor rows c0.., columns [c0, c0 + w) of the super-panel d (device,
+        ld lda) in place with the device driver (qrb_factorize on a view handle:
+        CholeskyQR2 panels, merged pairs, look-ahead); keep tau, T and the merged
+        pair reflectors for the later left-looking streams."""
+        nb, w2 = self.nb, 2 * self.nb
+        h = ctypes.c_void_p()
+        _native.check(self.lib.qrb_create_view(self.device, self.m - c0, w, nb, _p(d, c0),
+                                               self.lda, ctypes.byref(h)), "qrb_create_view")
+        try:
+            rep = _native.QrbReport()
+            _native.check(self.lib.qrb_factorize(h, ctypes.byref(rep)), "qrb_factorize")
+            k0 = c0 // nb
+            _native.check(self.lib.qrb_get_factors(h, _p(self.tau, c0),
+                                                   _p(self.t_all, k0 * nb * nb), nb),
+                          "qrb_get_factors")
+            npairs = (-(-w // nb)) // 2
+            if npairs:
+                _native.check(self.lib.qrb_get_pair_factors(
+                    h, _p(self.t2_all, (c0 // w2) * w2 * w2), w2), "qrb_get_pair_factors")
+                pairs_on = _native.get_tuning("outer_panels") >= 2
+                for p in range(npairs):
+                    # qrb_api.cu pair_ok: both panels full and 2nb rows below
+                    self.pair_valid[c0 // w2 + p] = (pairs_on and (p + 1) * w2 <= w
+                                                     and self.m - c0 - p * w2 >= w2)
+        finally:
+            self.lib.qrb_destroy(h)
+
+
+class HostStagedQR(_StagedFactors):
     """QR of an m x n matrix held in a pinned host torch tensor of shape (n, lda)
     (column-major, factored in place), using at most ``budget_bytes`` of HBM for
-    the super-panel (plus two reflector staging buffers)."""
+    the super-panel (plus two pair-wide reflector staging buffers).
+
+    In-core steps run the full device driver (qrb_factorize on a view handle of
+    the super-panel: CholeskyQR2 panels, merged panel pairs, look-ahead); the
+    left-looking stream applies earlier panels two at a time with their merged
+    2nb x 2nb reflectors (qrb_get_pair_factors), K = 2nb GEMMs."""
 
     def __init__(self, a_host, m: int, n: int, nb: int = 128, budget_bytes: int = 32 << 30):
         import torch
@@ -54,59 +142,54 @@ class HostStagedQR:
         self.a = a_host
         self.m, self.n, self.nb = m, n, nb
         self.lda = a_host.shape[1]
+        if self.lda % 2:
+            raise ValueError("the host matrix's leading dimension must be even")
         self.npan = -(-n // nb)
-        col_bytes = 8 * self.lda
-        stage_bytes = 2 * col_bytes * nb
-        sp_panels = max(1, (int(budget_bytes) - stage_bytes) // (col_bytes * nb))
-        self.sp_cols = min(n, sp_panels * nb)
-        dev = torch.device("cuda")
-        self.t_all = torch.zeros((self.npan * nb, nb), dtype=torch.float64, device=dev)
-        self.tau = torch.zeros(self.npan * nb, dtype=torch.float64, device=dev)
+        self.sp_cols = self.super_panel_cols(n, nb, self.lda, budget_bytes)
+        self._init_factors(torch.device("cuda"))
         self.copy_stream = torch.cuda.Stream()
         self.stats: dict = {}
 
     # -- helpers --------------------------------------------------------------------
-    def _stage_v(self, k: int, dst, stream) -> None:
-        """H2D of reflector panel k (rows j0.., pw columns) into dst (ld = lda)."""
+    def _stage_v(self, k: int, width: int, dst, stream) -> None:
+        """H2D of reflector columns [k nb, k nb + width) (rows j0..) into dst (ld = lda)."""
         j0 = k * self.nb
-        pw = min(self.nb, self.n - j0)
         st = self.lib.qrb_copy_2d(_p(dst), self.lda, _p(self.a, j0 + j0 * self.lda), self.lda,
-                                  self.m - j0, pw, 0, ctypes.c_void_p(stream.cuda_stream))
+                                  self.m - j0, width, 0, ctypes.c_void_p(stream.cuda_stream))
         _native.check(st, "qrb_copy_2d")
 
-    def _apply(self, k: int, v, c, c_row_off: int, ncols: int) -> None:
-        j0 = k * self.nb
-        pw = min(self.nb, self.n - j0)
-        st = self.lib.qrb_op_apply_qt(_p(v), self.lda, self.m - j0, pw,
-                                      _p(self.t_all, k * self.nb * self.nb), self.nb,
-                                      _p(c, c_row_off), self.lda, ncols, None)
-        _native.check(st, "qrb_op_apply_qt")
-
-    def _stream_previous(self, c, upto: int, vbufs, col_count: int, row_base=0) -> None:
-        """Apply Q_k^T for k < upto to the device block c (cols col_count)."""
+    def _stream_previous(self, c, upto: int, vbufs, col_count: int, row_base=0) -> int:
+        """Apply Q_k^T for panels k < upto to the device block c (cols col_count),
+        reflectors streamed from the host double-buffered; returns H2D bytes."""
         import torch
 
+        blocks = list(self._blocks(upto))
+        if not blocks:
+            return 0
         cur = torch.cuda.current_stream()
         done = [torch.cuda.Event(), torch.cuda.Event()]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
-        if upto <= 0:
-            return
+        moved = 0
         self.copy_stream.wait_stream(cur)
         with torch.cuda.stream(self.copy_stream):
-            self._stage_v(0, vbufs[0], self.copy_stream)
+            k, np_ = blocks[0]
+            self._stage_v(k, self._block_width(k, np_), vbufs[0], self.copy_stream)
             ready[0].record(self.copy_stream)
-        for k in range(upto):
-            b = k % 2
-            if k + 1 < upto:
-                nb_ = (k + 1) % 2
+        for i, (k, np_) in enumerate(blocks):
+            b = i % 2
+            if i + 1 < len(blocks):
+                nb_ = (i + 1) % 2
+                k1, np1 = blocks[i + 1]
                 with torch.cuda.stream(self.copy_stream):
-                    if k >= 1:
+                    if i >= 1:
                         self.copy_stream.wait_event(done[nb_])
-                    self._stage_v(k + 1, vbufs[nb_], self.copy_stream)
+                    self._stage_v(k1, self._block_width(k1, np1), vbufs[nb_], self.copy_stream)
                     ready[nb_].record(self.copy_stream)
             cur.wait_event(ready[b])
-            self._apply(k, vbufs[b], c, row_base + k * self.nb, col_count)
+            self._apply_block(k, np_, vbufs[b], 0, c, row_base + k * self.nb, col_count)
             done[b].record(cur)
+            moved += 8 * (self.m - k * self.nb) * self._block_width(k, np_)
+        return moved
 
     # -- factorization ------------------------------------------------------------------
     def factorize(self) -> dict:
@@ -115,42 +198,33 @@ class HostStagedQR:
         m, n, nb, lda = self.m, self.n, self.nb, self.lda
         dev = torch.device("cuda")
         d = torch.empty((self.sp_cols, lda), dtype=torch.float64, device=dev)
-        vbufs = [torch.empty((nb, lda), dtype=torch.float64, device=dev) for _ in range(2)]
+        vbufs = [torch.empty((2 * nb, lda), dtype=torch.float64, device=dev) for _ in range(2)]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h2d = d2h = 0
+        h2d = d2h = v_bytes = 0
+        in_core_s = 0.0
         for c0 in range(0, n, self.sp_cols):
             c1 = min(n, c0 + self.sp_cols)
             w = c1 - c0
             d[:w].copy_(self.a[c0:c1], non_blocking=True)
             h2d += 8 * w * lda
             # left-looking: every earlier panel's reflectors, streamed from the host
-            k0 = c0 // nb
-            self._stream_previous(d, k0, vbufs, w)
-            h2d += sum(8 * (m - k * nb) * min(nb, n - k * nb) for k in range(k0))
-            # right-looking inside the super-panel
-            for k in range(k0, -(-c1 // nb)):
-                j0 = k * nb
-                pw = min(nb, n - j0)
-                lc = j0 - c0
-                st = self.lib.qrb_op_panel(_p(d, j0 + lc * lda), lda, m - j0, pw,
-                                           _p(self.tau, j0), _p(self.t_all, k * nb * nb), nb,
-                                           None)
-                _native.check(st, "qrb_op_panel")
-                rest = w - (lc + pw)
-                if rest > 0:
-                    st = self.lib.qrb_op_apply_qt(_p(d, j0 + lc * lda), lda, m - j0, pw,
-                                                  _p(self.t_all, k * nb * nb), nb,
-                                                  _p(d, j0 + (lc + pw) * lda), lda, rest, None)
-                    _native.check(st, "qrb_op_apply_qt")
+            v_bytes += self._stream_previous(d, c0 // nb, vbufs, w)
+            # right-looking inside the super-panel (the device driver)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            self._factor_in_core(d, c0, w)
+            in_core_s += time.perf_counter() - t1
             self.a[c0:c1].copy_(d[:w], non_blocking=True)
             d2h += 8 * w * lda
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
+        del d, vbufs
         fl = 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
-        self.stats = {"seconds": secs, "tflops": fl / secs / 1e12, "h2d_bytes": h2d,
-                      "d2h_bytes": d2h, "super_panels": -(-n // self.sp_cols),
-                      "super_panel_cols": self.sp_cols}
+        self.stats = {"seconds": secs, "tflops": fl / secs / 1e12, "h2d_bytes": h2d + v_bytes,
+                      "d2h_bytes": d2h, "v_stream_bytes": v_bytes,
+                      "super_panels": -(-n // self.sp_cols), "super_panel_cols": self.sp_cols,
+                      "in_core_s": in_core_s}
         return self.stats
 
     # -- solve ------------------------------------------------------------------------------
@@ -170,7 +244,7 @@ class HostStagedQR:
         s = b_dev.shape[0]
         y = b_dev.clone()
         dev = torch.device("cuda")
-        vbufs = [torch.empty((nb, lda), dtype=torch.float64, device=dev) for _ in range(2)]
+        vbufs = [torch.empty((2 * nb, lda), dtype=torch.float64, device=dev) for _ in range(2)]
         self._stream_previous(y, self.npan, vbufs, s)
         resid = torch.linalg.norm(y[:, n:m], dim=1)
         # back substitution, bottom-up block columns of R streamed from the host

@@ -9,9 +9,9 @@ from oracle import tiled_qr as orc
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("m,n,sp_panels,nb", [(3000, 2000, 4, 128), (1500, 1500, 1, 64),
-                                                (2500, 700, 3, 32)])
-def test_host_staged_matches_oracle(m, n, sp_panels, nb):
+@pytest.mark.parametrize("m,n,sp_pairs,nb", [(3000, 2000, 2, 128), (1500, 1500, 1, 64),
+                                               (2500, 700, 3, 32), (2600, 2330, 3, 128)])
+def test_host_staged_matches_oracle(m, n, sp_pairs, nb):
     import torch
     from paper_1907_01891_b200.ooc import HostStagedQR
 
@@ -23,8 +23,9 @@ def test_host_staged_matches_oracle(m, n, sp_panels, nb):
     a_host = torch.zeros((n, lda), dtype=torch.float64, pin_memory=True)
     a_host[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T))
     col_bytes = 8 * lda
-    q = HostStagedQR(a_host, m, n, nb=nb, budget_bytes=(sp_panels + 2) * col_bytes * nb)
-    assert q.sp_cols == min(n, sp_panels * nb)
+    # budget: the super-panel (a whole number of panel pairs) + two pair-wide V buffers
+    q = HostStagedQR(a_host, m, n, nb=nb, budget_bytes=(2 * sp_pairs + 4) * col_bytes * nb)
+    assert q.sp_cols == min(n, sp_pairs * 2 * nb)
     st = q.factorize()
     assert st["super_panels"] == -(-n // q.sp_cols)
     f = orc.factorize_dense(a, 256, 64)
