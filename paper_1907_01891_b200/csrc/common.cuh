@@ -143,6 +143,12 @@ __device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const void* ss
                : "memory");
 }
 
+// bulk copy of `bytes` (multiple of 16) from shared to global memory
+__device__ __forceinline__ void bulk_store_f64(double* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

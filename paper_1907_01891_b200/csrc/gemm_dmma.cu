@@ -633,10 +633,14 @@ constexpr int AE_SBUF = 1;  // staging buffers (the bulk read of one finishes lo
 constexpr int AE_THREADS = (CONSUMER_WARPS + 2) * 32;  // + producer warp + epilogue warp
 constexpr int AE_SMEM = AE_STAGES * NN_STAGE_BYTES + AE_SBUF * RA_STAGING + 1024 + 256;
 
-__global__ void __launch_bounds__(AE_THREADS, 1)
-    gemm_nn_sub_asyncepi(const __grid_constant__ CUtensorMap mapA,
-                         const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
-                         const int64_t ldc, const NnArgs args) {
+// STORE = false: C -= A B (bulk L2 reduce-add of -acc);
+// STORE = true:  C = A B   (bulk copy of +acc: the panel chain's K = nb products
+// Q1 = P R1^-1 and V = Q1 M, where the one-tile-per-CTA kernel spent ~30% of
+// every tile in its prologue and epilogue)
+template <bool STORE>
+__device__ __forceinline__ void nn_asyncepi_body(const CUtensorMap& mapA, const CUtensorMap& mapB,
+                                                 double* __restrict__ C, const int64_t ldc,
+                                                 const NnArgs& args) {
   if (pred_off(args.pred)) return;
   constexpr int NT = NN_BN / 16;
   extern __shared__ uint8_t smem_raw[];
@@ -706,10 +710,14 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
         if (ng0 + n < args.N && rows > 0) {
           double* dst = C + mg0 + static_cast<int64_t>(ng0 + n) * ldc;
           const int even = rows & ~1;
-          if (even) bulk_reduce_add_f64(dst, stage + n * RA_COL_BYTES, even * 8);
-          if (rows & 1)
-            atomicAdd(dst + even,
-                      *reinterpret_cast<const double*>(stage + n * RA_COL_BYTES + even * 8));
+          const double* src = reinterpret_cast<const double*>(stage + n * RA_COL_BYTES);
+          if (STORE) {
+            if (even) bulk_store_f64(dst, src, even * 8);
+            if (rows & 1) dst[even] = src[even];
+          } else {
+            if (even) bulk_reduce_add_f64(dst, src, even * 8);
+            if (rows & 1) atomicAdd(dst + even, src[even]);
+          }
         }
       }
       bulk_commit();
@@ -782,7 +790,9 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
           // -acc by flipping the sign bits on the integer pipe (a DADD would
           // occupy the FP64 pipe the DMMAs share)
           *reinterpret_cast<double2*>(stage + n * RA_COL_BYTES + m * 8) =
-              make_double2(neg_bits(acc[mp * 2 + 0][nt][e]), neg_bits(acc[mp * 2 + 1][nt][e]));
+              STORE ? make_double2(acc[mp * 2 + 0][nt][e], acc[mp * 2 + 1][nt][e])
+                    : make_double2(neg_bits(acc[mp * 2 + 0][nt][e]),
+                                   neg_bits(acc[mp * 2 + 1][nt][e]));
         }
       }
     }
@@ -790,6 +800,20 @@ __global__ void __launch_bounds__(AE_THREADS, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&sfull[sb]);
   }
+}
+
+__global__ void __launch_bounds__(AE_THREADS, 1)
+    gemm_nn_sub_asyncepi(const __grid_constant__ CUtensorMap mapA,
+                         const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
+                         const int64_t ldc, const NnArgs args) {
+  nn_asyncepi_body<false>(mapA, mapB, C, ldc, args);
+}
+
+__global__ void __launch_bounds__(AE_THREADS, 1)
+    gemm_nn_store_asyncepi(const __grid_constant__ CUtensorMap mapA,
+                           const __grid_constant__ CUtensorMap mapB, double* __restrict__ C,
+                           const int64_t ldc, const NnArgs args) {
+  nn_asyncepi_body<true>(mapA, mapB, C, ldc, args);
 }
 
 // Same kernel with dynamic tile tickets (first tile static, then a per-launch
@@ -1244,6 +1268,32 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
   }
   if (epi == GEMM_EPI_SUB)
     return launch<false, 64, GEMM_EPI_SUB>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
+  {
+    // C = A B with more tiles than SMs: persistent, async bulk-store epilogue
+    const int num_m = (M + BM - 1) / BM;
+    const int num_n = (N + NN_BN - 1) / NN_BN;
+    static const bool store_persistent = std::getenv("QRB_NN_STORE_CLASSIC") == nullptr;
+    if (store_persistent && num_m * num_n > gemm_sm_count()) {
+      QRB_TRY(set_max_dynamic_smem(reinterpret_cast<const void*>(gemm_nn_store_asyncepi), AE_SMEM));
+      CUtensorMap ma, mb;
+      QRB_TRY(make_map(&ma, a_mm, 16, BK));
+      QRB_TRY(make_map(&mb, b, BK, NN_BN));
+      NnArgs args{};
+      args.pred = launch_pred();
+      args.M = M;
+      args.N = N;
+      args.K = K;
+      args.mask_a = mask_a;
+      args.group_m = 16;
+      args.num_tiles = num_m * num_n;
+      const int cap = gemm_grid_cap();
+      const int grid =
+          std::min(args.num_tiles, cap > 0 ? std::min(cap, gemm_sm_count()) : gemm_sm_count());
+      gemm_nn_store_asyncepi<<<grid, AE_THREADS, AE_SMEM, stream>>>(ma, mb, out, ldo, args);
+      QRB_CUDA_TRY(cudaGetLastError());
+      return QRB_OK;
+    }
+  }
   return launch<false, 64, GEMM_EPI_STORE>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
 }
 
