@@ -53,7 +53,10 @@ class DiskStagedQR(_StagedFactors):
     super-panel.  ``src`` may be None when only solving with existing factors."""
 
     def __init__(self, src: TiledMatrix | None, dst: TiledMatrix, nb: int = 128,
-                 budget_bytes: int = 32 << 30, io_threads: int = 2):
+                 budget_bytes: int = 32 << 30, io_threads: int = 2, page_cache: bool = True):
+        """``page_cache=False``: every read comes from the device and every write
+        is synced to it and dropped from the OS page cache (TiledMatrix.uncached)
+        -- how the engine behaves when the host has no RAM to spare for caching."""
         import torch
 
         m, n = dst.rows, dst.cols
@@ -63,6 +66,9 @@ class DiskStagedQR(_StagedFactors):
             raise ValueError("source and factor stores differ in shape")
         self.lib = _native.load()
         self.src, self.dst = src, dst
+        for st in (src, dst):
+            if st is not None:
+                st.uncached = not page_cache
         self.m, self.n, self.nb = m, n, nb
         self.lda = (m + 31) // 32 * 32
         self.npan = -(-n // nb)

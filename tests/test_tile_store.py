@@ -97,3 +97,19 @@ def test_cache_lru_pins_and_flush(tmp_path):
     c.flush()
     assert not m.load_tile(TileId(0, 0)).any()
     assert c.writes_to_disk == 1
+
+
+def test_uncached_column_io_roundtrip(tmp_path):
+    """Page-cache-bypassing column I/O (the disk tier's uncached mode) moves the
+    same bytes as the cached path."""
+    from paper_1907_01891_b200.tile_store import TiledMatrix
+    rng = np.random.default_rng(4)
+    m, n, b = 70, 45, 16
+    a = rng.standard_normal((m, n))
+    t = TiledMatrix.create(m, n, b, tmp_path / "u")
+    t.uncached = True
+    t.write_columns(0, n, np.asfortranarray(a))
+    out = np.zeros((m, 20), order="F")
+    t.read_columns(13, 20, 5, out)
+    np.testing.assert_array_equal(out[5:], a[5:, 13:33])
+    assert not out[:5].any()
