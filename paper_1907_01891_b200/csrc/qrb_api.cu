@@ -715,6 +715,9 @@ struct qrb_handle {
   double* T2 = nullptr;    // merged 2nb x 2nb reflectors of panel pairs (kept from the
   bool t2_ready = false;   //   factorization's pair steps, the rest filled at the first solve)
   std::vector<char> t2_valid;
+  double* T4 = nullptr;    // merged 4nb x 4nb reflectors of panel quads (4q .. 4q+3): kept
+  std::vector<char> t4_valid;  //   from the factorization's 4-panel blocks, the rest at the
+  bool t4_ready = false;       //   first solve (Q^T B with K = 4nb GEMMs)
   double* Rinv2 = nullptr; // inverses of the 2nb x 2nb diagonal blocks of R (pairs), lazily
   bool rinv2_ready = false;
   DevBuf Ytmp;             // copy of a 2nb-row block of the right-hand sides
@@ -736,6 +739,7 @@ struct qrb_handle {
   uint64_t fgraph_epoch = 0;
   int64_t fgraph_launches = 0;
   std::vector<char> fgraph_t2;  // t2_valid as the captured run leaves it
+  std::vector<char> fgraph_t4;
   bool fgraph_warm = false;     // one eager run first (sizes every buffer)
 };
 
@@ -802,7 +806,9 @@ void invalidate_derived(qrb_handle* h) {
   h->rinv_ready = false;
   h->t2_ready = false;
   h->rinv2_ready = false;
+  h->t4_ready = false;
   std::fill(h->t2_valid.begin(), h->t2_valid.end(), 0);
+  std::fill(h->t4_valid.begin(), h->t4_valid.end(), 0);
 }
 
 // merged 2nb-wide reflectors of panel pairs (2p, 2p+1), for the solve's Q^T B
@@ -812,10 +818,21 @@ bool pair_ok(const qrb_handle* h, int k) {
          h->m - j0 >= 2 * int64_t(h->nb);
 }
 
+// right-hand-side batches from this width on merge the quad reflectors the
+// factorization did not keep (qrb_set_tuning "t4_min_rhs")
+static int64_t g_t4_min_rhs = 1024;
+
+// merged 4nb-wide reflectors of panel quads (4q .. 4q+3)
+bool quad_ok(const qrb_handle* h, int k) {
+  const int64_t j0 = int64_t(k) * h->nb, w4 = 4 * int64_t(h->nb);
+  return g_outer_panels >= 4 && (k & 3) == 0 && j0 + w4 <= h->n && h->m - j0 >= w4;
+}
+
 // storage of the merged pair reflectors (npairs blocks of 2nb x 2nb + scratch)
+// and of the quad reflectors (nquads blocks of 4nb x 4nb)
 int t2_storage(qrb_handle* h) {
-  const int64_t w2 = 2 * int64_t(h->nb), blk = w2 * w2;
-  const int npairs = h->npanels / 2;
+  const int64_t w2 = 2 * int64_t(h->nb), blk = w2 * w2, blk4 = 4 * blk;
+  const int npairs = h->npanels / 2, nquads = h->npanels / 4;
   if (!h->T2 && npairs > 0) {
     if (cudaMalloc(&h->T2, sizeof(double) * (npairs * blk + 2 * int64_t(h->nb) * h->nb)) !=
         cudaSuccess) {
@@ -824,8 +841,19 @@ int t2_storage(qrb_handle* h) {
       set_last_error("T2 alloc failed");
       return QRB_ENOMEM;
     }
+    ++g_graph_epoch;
+  }
+  if (!h->T4 && nquads > 0) {
+    if (cudaMalloc(&h->T4, sizeof(double) * nquads * blk4) != cudaSuccess) {
+      cudaGetLastError();
+      h->T4 = nullptr;
+      set_last_error("T4 alloc failed");
+      return QRB_ENOMEM;
+    }
+    ++g_graph_epoch;
   }
   h->t2_valid.assign(npairs, 0);
+  h->t4_valid.assign(nquads, 0);
   return QRB_OK;
 }
 
@@ -849,6 +877,27 @@ int ensure_t2(qrb_handle* h, Workspace& ws) {
     h->t2_valid[p] = 1;
   }
   h->t2_ready = true;
+  return QRB_OK;
+}
+
+// quad reflectors the factorization did not keep (its pair steps), merged from
+// the pair reflectors: T4 = [[T2a, -T2a (V_a^T V_b) T2b], [0, T2b]]
+int ensure_t4(qrb_handle* h, Workspace& ws) {
+  if (h->t4_ready) return QRB_OK;
+  QRB_TRY(ensure_t2(h, ws));
+  const int nb = h->nb;
+  const int64_t w2 = 2 * int64_t(nb), blk2 = w2 * w2, w4 = 2 * w2, blk4 = w4 * w4;
+  const int nquads = h->npanels / 4;
+  MatView A{h->A, h->m, h->n, h->lda};
+  for (int q = 0; q < nquads; ++q) {
+    if (!quad_ok(h, 4 * q) || h->t4_valid[q]) continue;
+    QRB_TRY(ws.T4.ensure(sizeof(double) * 2 * blk2, h->stream));
+    QRB_TRY(merge_pair_t(A, int64_t(4 * q) * nb, static_cast<int>(w2),
+                         h->T2 + int64_t(2 * q) * blk2, h->T2 + int64_t(2 * q + 1) * blk2,
+                         h->T4 + q * blk4, w4, ws.T4.d(), ws, h->stream));
+    h->t4_valid[q] = 1;
+  }
+  h->t4_ready = true;
   return QRB_OK;
 }
 
@@ -890,7 +939,10 @@ int ensure_rinv2(qrb_handle* h) {
 }
 
 // B (n x nrhs) <- R^-1 B, bottom-up: panel pairs as 2nb blocks (inverse block +
-// rank-2nb update, K = 2nb GEMMs), single nb blocks where no full pair exists
+// rank-2nb update, K = 2nb GEMMs), single nb blocks where no full pair exists.
+// (4nb blocks -- the two pair inverses with the coupling block between them,
+// then one K = 4nb update -- measured 38.1 -> 40.0 ms for 256 slices at config 3:
+// the unsplit 256 x 256 coupling product costs more than the wider update saves)
 int trsm_upper_h(qrb_handle* h, const MatView& B, cudaStream_t st) {
   const int nb = h->nb;
   const int64_t n = h->n, nrhs = B.cols;
@@ -899,35 +951,44 @@ int trsm_upper_h(qrb_handle* h, const MatView& B, cudaStream_t st) {
                8.0 * (0.5 * n * (double)n + 2.0 * n * (double)nrhs), st);
   MatView R{h->A, n, n, h->lda};
   const int64_t w2 = 2 * int64_t(nb);
+  // Y_kb <- D Y_kb for the pair starting at panel kb (D = its 2nb x 2nb inverse)
+  auto pair_diag = [&](int kb) -> int {
+    const int64_t i0 = int64_t(kb) * nb;
+    const int64_t bs = w2;
+    MatView Yk = B.sub(i0, 0, bs, nrhs);
+    const MatView D{h->Rinv2 + int64_t(kb / 2) * w2 * w2, bs, bs, w2};
+    const int s2 = small_splits(static_cast<int>(bs), static_cast<int>(nrhs), static_cast<int>(bs));
+    if (s2 > 1) {
+      // Y_k <- D Y_k as split-K partial products reduced into Y_k (few output tiles)
+      QRB_TRY(small_product(false, D, Yk, Yk.ptr, Yk.ld, static_cast<int>(bs),
+                            static_cast<int>(nrhs), static_cast<int>(bs), s2, device_workspace(),
+                            st));
+      return QRB_OK;
+    }
+    // Y_k <- D Y_k through a copy (M = 2nb spans two row tiles: no in-place GEMM)
+    const int64_t ldt = w2;
+    QRB_TRY(h->Ytmp.ensure(sizeof(double) * ldt * nrhs, st));
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(h->Ytmp.d(), sizeof(double) * ldt, Yk.ptr,
+                                   sizeof(double) * Yk.ld, sizeof(double) * bs, nrhs,
+                                   cudaMemcpyDeviceToDevice, st));
+    QRB_TRY(gemm_nn(D, MatView{h->Ytmp.d(), bs, nrhs, ldt}, Yk.ptr, Yk.ld, bs, nrhs, bs,
+                    GEMM_EPI_STORE, 0, st));
+    g_launches += 1;
+    return QRB_OK;
+  };
   for (int k = h->npanels - 1; k >= 0;) {
     const bool pair = (k & 1) && pair_ok(h, k - 1);
     const int kb = pair ? k - 1 : k;
     const int64_t i0 = int64_t(kb) * nb;
     const int64_t bs = pair ? w2 : std::min<int64_t>(nb, n - i0);
     MatView Yk = B.sub(i0, 0, bs, nrhs);
-    const int s2 = pair ? small_splits(static_cast<int>(bs), static_cast<int>(nrhs),
-                                       static_cast<int>(bs)) : 1;
-    if (pair && s2 > 1) {
-      // Y_k <- D Y_k as split-K partial products reduced into Y_k (few output tiles)
-      QRB_TRY(small_product(false, MatView{h->Rinv2 + int64_t(kb / 2) * w2 * w2, bs, bs, w2}, Yk,
-                            Yk.ptr, Yk.ld, static_cast<int>(bs), static_cast<int>(nrhs),
-                            static_cast<int>(bs), s2, device_workspace(), st));
-      g_launches -= 1;
-    } else if (pair) {
-      // Y_k <- D Y_k through a copy (M = 2nb spans two row tiles: no in-place GEMM)
-      const int64_t ldt = w2;
-      QRB_TRY(h->Ytmp.ensure(sizeof(double) * ldt * nrhs, st));
-      QRB_CUDA_TRY(cudaMemcpy2DAsync(h->Ytmp.d(), sizeof(double) * ldt, Yk.ptr,
-                                     sizeof(double) * Yk.ld, sizeof(double) * bs, nrhs,
-                                     cudaMemcpyDeviceToDevice, st));
-      QRB_TRY(gemm_nn(MatView{h->Rinv2 + int64_t(kb / 2) * w2 * w2, bs, bs, w2},
-                      MatView{h->Ytmp.d(), bs, nrhs, ldt}, Yk.ptr, Yk.ld, bs, nrhs, bs,
-                      GEMM_EPI_STORE, 0, st));
+    if (pair) {
+      QRB_TRY(pair_diag(kb));
     } else {
       MatView Ri{h->Rinv + int64_t(kb) * nb * nb, bs, bs, nb};
       QRB_TRY(gemm_nn(Ri, Yk, Yk.ptr, Yk.ld, bs, nrhs, bs, GEMM_EPI_STORE, 0, st));
+      g_launches += 1;
     }
-    g_launches += 1;
     if (i0 > 0) {
       MatView Rk = R.sub(0, i0, i0, bs);
       QRB_TRY(gemm_nn(Rk, Yk, B.ptr, B.ld, i0, nrhs, bs, GEMM_EPI_SUB, 0, st));
@@ -1022,8 +1083,11 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
                               t2dst(j0 + w2)));
     t2mark(j0 + w2);
     QRB_TRY(wsb.T4.ensure(sizeof(double) * 2 * blk2, sb));
-    double* T4 = h->T4scratch.d() + ((j0 / wq) & 1) * blkq;
+    // quad-aligned blocks keep their merged reflector for the solve
+    const bool keep = h->T4 && j0 % wq == 0 && quad_ok(h, static_cast<int>(j0 / nb));
+    double* T4 = keep ? h->T4 + (j0 / wq) * blkq : h->T4scratch.d() + ((j0 / wq) & 1) * blkq;
     QRB_TRY(merge_pair_t(A, j0, static_cast<int>(w2), T2a, T2b, T4, wq, wsb.T4.d(), wsb, sb));
+    if (keep) h->t4_valid[j0 / wq] = 1;
     *Tout = T4;
     return QRB_OK;
   };
@@ -1130,6 +1194,7 @@ static int factorize_graphed(qrb_handle* h, Workspace& ws, cudaStream_t st) {
     QRB_CUDA_TRY(cudaGraphLaunch(h->fgraph, st));
     g_launches += h->fgraph_launches;
     h->t2_valid = h->fgraph_t2;
+    h->t4_valid = h->fgraph_t4;
     return QRB_OK;
   }
   if (h->fgraph) {
@@ -1166,6 +1231,7 @@ static int factorize_graphed(qrb_handle* h, Workspace& ws, cudaStream_t st) {
   h->fgraph_epoch = g_graph_epoch.load() == epoch ? epoch : 0;
   h->fgraph_launches = g_launches.load() - l0;
   h->fgraph_t2 = h->t2_valid;
+  h->fgraph_t4 = h->t4_valid;
   ++g_graph_captures;
   QRB_CUDA_TRY(cudaGraphLaunch(exec, st));
   return QRB_OK;
@@ -1278,6 +1344,7 @@ int qrb_destroy(qrb_handle* h) {
   if (h->T) cudaFree(h->T);
   if (h->Rinv) cudaFree(h->Rinv);
   if (h->T2) cudaFree(h->T2);
+  if (h->T4) cudaFree(h->T4);
   if (h->Rinv2) cudaFree(h->Rinv2);
   h->Ytmp.release();
   h->Bw.release();
@@ -1697,12 +1764,23 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
   QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
   QRB_TRY(ensure_rinv(h));
   QRB_TRY(ensure_t2(h, ws));
+  // quad reflectors: the ones the factorization kept are free; merging the rest
+  // (one m_k x 2nb x 2nb product each) pays only for wide right-hand-side
+  // batches (config 2, 64 slices: 7.7 -> 9.3 ms with every quad merged per solve)
+  if (nrhs >= g_t4_min_rhs) QRB_TRY(ensure_t4(h, ws));
   MatView A{h->A, h->m, h->n, h->lda};
   MatView Bv{Bw, h->m, nrhs, ldw};
   for (int k = 0; k < h->npanels;) {
     const int64_t j0 = int64_t(k) * h->nb;
     const int64_t pw = std::min<int64_t>(h->nb, h->n - j0);
     const int64_t mk = h->m - j0;
+    if (quad_ok(h, k) && h->t4_valid[k / 4]) {  // four panels at once (K = 4nb)
+      const int64_t w4 = 4 * int64_t(h->nb);
+      QRB_TRY(apply_qt(A.sub(j0, j0, mk, w4), h->T4 + int64_t(k / 4) * w4 * w4, w4,
+                       Bv.sub(j0, 0, mk, nrhs), ws, st));
+      k += 4;
+      continue;
+    }
     if (pair_ok(h, k)) {  // two panels at once with the merged reflector (K = 2nb)
       const int64_t w2 = 2 * int64_t(h->nb);
       QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), h->T2 + int64_t(k / 2) * w2 * w2, w2,
@@ -1991,6 +2069,10 @@ int64_t qrb_launch_count(void) { return g_launches.load(); }
 int qrb_set_tuning(const char* key, int64_t value) {
   const std::string k = key ? key : "";
   ++g_graph_epoch;  // captured factorization graphs bake the knobs in
+  if (k == "t4_min_rhs" && value >= 0) {
+    g_t4_min_rhs = value;
+    return QRB_OK;
+  }
   if (k == "graph_max_cols" && value >= 0) {
     g_graph_max_cols = value;
     return QRB_OK;
@@ -2065,6 +2147,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
   else if (k == "cholqr_fallbacks") *value = cholqr_fallback_count();
   else if (k == "graph_max_cols") *value = g_graph_max_cols;
+  else if (k == "t4_min_rhs") *value = g_t4_min_rhs;
   else if (k == "graph_captures") *value = g_graph_captures.load();
   else if (k == "graph_replays") *value = g_graph_replays.load();
   else {

@@ -310,3 +310,37 @@ def test_apply_qt_cols_rejects_a_replaced_workspace():
     assert lib.qrb_op_apply_qt(p(v), m, m, w, p(t), w, p(c2), m, nc, None) == 0   # new W2
     assert lib.qrb_op_apply_qt_cols(p(v), m, m, w, p(c), m, 32, 32, None) == _native.QRB_ESTATE
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("outer4_min_cols,t4_min_rhs", [(0, 1 << 30), (0, 0), (1 << 30, 0)])
+def test_solve_with_quad_reflectors_matches_oracle(outer4_min_cols, t4_min_rhs):
+    """Q^T B four panels at a time (merged 4nb x 4nb reflectors, K = 4nb GEMMs):
+    the quads the factorization kept (4-panel blocks forced at this size), the
+    quads merged at solve time, and both mixed with pairs -- all against the
+    oracle's solution and residuals (kernels.py:324-341 applies one panel at a
+    time)."""
+    from oracle.tiled_qr import factorize_dense, residual_norms, solve_dense
+    from paper_1907_01891_b200 import _native
+    from paper_1907_01891_b200.device import QrDevice
+    from conftest import rel_err
+    rng = np.random.default_rng(41)
+    m, n = 3300, 2944                      # 23 panels: 5 quads + a pair + a single
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.linspace(40, 1, n)) @ v.T
+    b = rng.standard_normal((m, 7))
+    keys = {k: _native.get_tuning(k) for k in ("outer4_min_cols", "t4_min_rhs", "outer_panels")}
+    try:
+        _native.set_tuning("outer_panels", 4)
+        _native.set_tuning("outer4_min_cols", outer4_min_cols)
+        _native.set_tuning("t4_min_rhs", t4_min_rhs)
+        with QrDevice(m, n) as q:
+            q.set_matrix(a)
+            q.factorize()
+            x, resid, _ = q.solve(b)
+    finally:
+        for k, v_ in keys.items():
+            _native.set_tuning(k, v_)
+    f = factorize_dense(a, 512, 128)
+    assert rel_err(x, solve_dense(f, b)) <= 1e-8
+    np.testing.assert_allclose(resid, residual_norms(f, b), rtol=1e-9)
