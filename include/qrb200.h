@@ -145,6 +145,29 @@ QRB_API int qrb_factorize(qrb_handle* h, qrb_report* rep);
 QRB_API int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
                                qrb_report* rep);
 
+/* qrb_factorize_host while the caller is still filling src: the column chunk c
+ * (columns [c*chunk_cols, (c+1)*chunk_cols), chunk_cols a multiple of nb) is
+ * copied only once ready[c] > 0 (a host int32 per chunk, set by the caller's
+ * reader threads after the chunk's columns are in src; ready[c] < 0 aborts the
+ * call with QRB_EARG -- the caller could not read the chunk).  progress (optional,
+ * page-locked mapped host int64): the library keeps storing there, in stream
+ * order, how many leading columns are final, so the caller can stream finished
+ * columns out (qrb_get_matrix_async) while the factorization runs.  The first chunks are
+ * factored left-looking while later ones are still being read; input_gbps is the
+ * arrival rate assumed for switching to the right-looking order (0 = PCIe).
+ * Replaces the reference's overlapped mode (one prefetching I/O agent feeding
+ * the tile tasks, task_engine.py:330-474) for the in-HBM drop-in factorize. */
+QRB_API int qrb_factorize_host_gated(qrb_handle* h, const double* src, int64_t ld,
+                                     int64_t chunk_cols, const int32_t* ready, double input_gbps,
+                                     int64_t* progress, qrb_report* rep);
+
+/* Columns [col0, col0+ncols) of the handle's matrix to dst on the caller's
+ * stream, without waiting (the caller orders it -- e.g. after *progress of
+ * qrb_factorize_host_gated covers the columns).  Replaces the reference's
+ * eager write-back of finished tiles by its I/O agent (task_engine.py:330-474). */
+QRB_API int qrb_get_matrix_async(qrb_handle* h, int64_t col0, int64_t ncols, double* dst,
+                                 int64_t ld, void* stream);
+
 /* Persisted-factor interop: tau (n) and the per-panel T factors
  * (nb x nb each, panel k at T + k*nb*ldt... stored as an nb x (npanels*nb) matrix). */
 QRB_API int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt);

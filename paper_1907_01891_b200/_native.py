@@ -79,6 +79,9 @@ SIGNATURES = {
     "qrb_set_stream": (c_int, [c_void_p, c_void_p]),
     "qrb_factorize": (c_int, [c_void_p, ctypes.POINTER(QrbReport)]),
     "qrb_factorize_host": (c_int, [c_void_p, c_void_p, c_i64, c_i64, ctypes.POINTER(QrbReport)]),
+    "qrb_factorize_host_gated": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p,
+                                         ctypes.c_double, c_void_p, ctypes.POINTER(QrbReport)]),
+    "qrb_get_matrix_async": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p]),
     "qrb_get_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_get_pair_factors": (c_int, [c_void_p, c_void_p, c_i64]),
     "qrb_set_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),

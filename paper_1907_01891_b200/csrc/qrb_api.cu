@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -668,6 +670,10 @@ static int trsm_upper(const MatView& R, const double* Rinv, int nb, const MatVie
   return QRB_OK;
 }
 
+// the factorization's progress for a caller streaming finished columns out
+// (qrb_factorize_host_gated): one thread stores into page-locked host memory
+__global__ void progress_kernel(volatile int64_t* p, int64_t v) { *p = v; }
+
 __global__ void nonfinite_kernel(const double* A, int64_t lda, int64_t m, int64_t n, int* flag) {
   const int64_t total = m * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -741,6 +747,8 @@ struct qrb_handle {
   std::vector<char> fgraph_t2;  // t2_valid as the captured run leaves it
   std::vector<char> fgraph_t4;
   bool fgraph_warm = false;     // one eager run first (sizes every buffer)
+  int64_t* progress = nullptr;  // device alias of a caller's page-locked counter: number of
+                                //   leading columns whose factored values are final
 };
 
 namespace {
@@ -1035,6 +1043,14 @@ static int64_t g_graph_max_cols = [] {
   return e ? std::atoll(e) : int64_t(16384);
 }();
 
+static int report_progress(qrb_handle* h, int64_t cols, cudaStream_t st) {
+  if (!h->progress) return QRB_OK;
+  progress_kernel<<<1, 1, 0, st>>>(h->progress, cols);
+  QRB_CUDA_TRY(cudaGetLastError());
+  g_launches += 1;
+  return QRB_OK;
+}
+
 static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_t st) {
   const int nb = h->nb;
   const int64_t m = h->m, n = h->n, w2 = 2 * int64_t(nb), blk2 = w2 * w2;
@@ -1111,6 +1127,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     if (w == 0) {
       const int64_t pw = std::min<int64_t>(nb, n - j0);
       QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st));
+      QRB_TRY(report_progress(h, j0 + pw, st));
       if (j0 + pw < n)
         QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, n - j0 - pw), ws,
                          st));
@@ -1119,6 +1136,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
       continue;
     }
     if (!have) QRB_TRY(factor_block(j0, static_cast<int>(w), ws, st, &TB));
+    QRB_TRY(report_progress(h, j0 + w, st));  // (a look-ahead block: st waited for it)
     have = 0;
     const int64_t c0 = j0 + w, rest = n - c0;
     const MatView V = A.sub(j0, j0, mk, w);
@@ -1398,6 +1416,20 @@ int qrb_set_matrix(qrb_handle* h, int64_t col0, int64_t ncols, const double* src
   return QRB_OK;
 }
 
+int qrb_get_matrix_async(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
+                         void* stream) {
+  if (!h || !dst || col0 < 0 || ncols < 0 || col0 + ncols > h->n || ld < h->m) {
+    set_last_error("qrb_get_matrix_async: bad arguments");
+    return QRB_EARG;
+  }
+  DeviceGuard g(h->device);
+  if (ncols == 0) return QRB_OK;
+  QRB_CUDA_TRY(cudaMemcpy2DAsync(dst, ld * sizeof(double), h->A + col0 * h->lda,
+                                 h->lda * sizeof(double), h->m * sizeof(double), ncols,
+                                 cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return QRB_OK;
+}
+
 int qrb_get_matrix(qrb_handle* h, int64_t col0, int64_t ncols, double* dst, int64_t ld,
                    int dst_on_device) {
   if (!h || !dst || col0 < 0 || ncols < 0 || col0 + ncols > h->n || ld < h->m) {
@@ -1504,10 +1536,11 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
 // ~34 TFLOP/s).  A function of the shape only, so the factors (and their
 // rounding) are the same every run; QRB_E2E_NO_SWITCH keeps the left-looking
 // order to the end.
-static int64_t host_switch_chunk(int64_t m, int64_t n, int64_t W, int64_t nchunks) {
+static int64_t host_switch_chunk(int64_t m, int64_t n, int64_t W, int64_t nchunks,
+                                 double input_gbps = 45.0) {
   static const bool no_switch = std::getenv("QRB_E2E_NO_SWITCH") != nullptr;
   if (no_switch) return nchunks;
-  const double copy_s = 8.0 * static_cast<double>(m) * n / 45e9;
+  const double copy_s = 8.0 * static_cast<double>(m) * n / (input_gbps * 1e9);
   double work_s = 0.0;
   for (int64_t c = 0; c < nchunks; ++c) {
     if (c > 0 && work_s >= copy_s) return c;
@@ -1518,8 +1551,13 @@ static int64_t host_switch_chunk(int64_t m, int64_t n, int64_t W, int64_t nchunk
   return nchunks;
 }
 
-int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
-                       qrb_report* rep) {
+// ready != nullptr: chunk c of src (columns [c W, c W + W)) may be read only once
+// ready[c] != 0 -- the caller is still filling src (e.g. from disk) while the
+// factorization runs; input_gbps is the rate the model of the left-looking ->
+// right-looking switch assumes for the arrival of the whole matrix.
+static int factorize_host_impl(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
+                               const volatile int32_t* ready, double input_gbps,
+                               int64_t* progress_host, qrb_report* rep) {
   clear_report(rep);
   if (!h || !src || ld < h->m || chunk_cols < 0) {
     set_last_error("qrb_factorize_host: bad arguments");
@@ -1536,7 +1574,8 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
   if (W == 0) W = 4096;  // measured best at config 3 (2048..32768 swept)
   W = std::max<int64_t>(nb, (W + nb - 1) / nb * nb);
   const int64_t nchunks = (h->n + W - 1) / W;
-  const int64_t c_switch = host_switch_chunk(h->m, h->n, W, nchunks);
+  const int64_t c_switch =
+      host_switch_chunk(h->m, h->n, W, nchunks, input_gbps > 0 ? input_gbps : 45.0);
   cudaStream_t cs = nullptr;
   std::vector<cudaEvent_t> landed(nchunks, nullptr);
   cudaEvent_t c0ev = nullptr, c1ev = nullptr;
@@ -1551,15 +1590,30 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     QRB_CUDA_TRY(cudaEventRecord(h->ev0, st));
     QRB_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev0, 0));
     QRB_CUDA_TRY(cudaEventRecord(c0ev, cs));
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int64_t col0 = c * W, nc = std::min(W, h->n - col0);
-      QRB_CUDA_TRY(cudaEventCreateWithFlags(&landed[c], cudaEventDisableTiming));
-      QRB_CUDA_TRY(cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double),
-                                     src + col0 * ld, ld * sizeof(double), h->m * sizeof(double),
-                                     nc, cudaMemcpyHostToDevice, cs));
-      QRB_CUDA_TRY(cudaEventRecord(landed[c], cs));
-    }
-    QRB_CUDA_TRY(cudaEventRecord(c1ev, cs));
+    // copies are enqueued in chunk order; gated chunks only once the caller has
+    // filled them (this thread waits, the GPU keeps working on queued chunks)
+    int64_t enq = 0;
+    auto copy_upto = [&](int64_t last) -> int {
+      for (; enq <= last && enq < nchunks; ++enq) {
+        const int64_t col0 = enq * W, nc = std::min(W, h->n - col0);
+        if (ready) {
+          while (ready[enq] == 0) std::this_thread::sleep_for(std::chrono::microseconds(50));
+          if (ready[enq] < 0) {  // the caller could not produce this chunk
+            set_last_error("qrb_factorize_host_gated: input chunk " + std::to_string(enq) +
+                           " reported unavailable");
+            return QRB_EARG;
+          }
+        }
+        QRB_CUDA_TRY(cudaEventCreateWithFlags(&landed[enq], cudaEventDisableTiming));
+        QRB_CUDA_TRY(cudaMemcpy2DAsync(h->A + col0 * h->lda, h->lda * sizeof(double),
+                                       src + col0 * ld, ld * sizeof(double),
+                                       h->m * sizeof(double), nc, cudaMemcpyHostToDevice, cs));
+        QRB_CUDA_TRY(cudaEventRecord(landed[enq], cs));
+        if (enq == nchunks - 1) QRB_CUDA_TRY(cudaEventRecord(c1ev, cs));
+      }
+      return QRB_OK;
+    };
+    if (!ready) QRB_TRY(copy_upto(nchunks - 1));
     MatView A{h->A, h->m, h->n, h->lda};
     QRB_TRY(t2_storage(h));
     // non-finite input check per landed chunk (flag read once at the end)
@@ -1592,6 +1646,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
         // right-looking order (the remaining columns catch up on every earlier
         // panel with wide GEMMs, then the usual panel + trailing-update steps)
         const int64_t rem = h->n - col0;
+        QRB_TRY(copy_upto(nchunks - 1));
         QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[nchunks - 1], 0));
         nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, rem, nf);
         QRB_CUDA_TRY(cudaGetLastError());
@@ -1600,6 +1655,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
         QRB_TRY(right_looking(h, col0, ws, st));
         break;
       }
+      QRB_TRY(copy_upto(c));
       QRB_CUDA_TRY(cudaStreamWaitEvent(st, landed[c], 0));
       nonfinite_kernel<<<4 * 148, 256, 0, st>>>(h->A + col0 * h->lda, h->lda, h->m, nc, nf);
       QRB_CUDA_TRY(cudaGetLastError());
@@ -1627,6 +1683,7 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
         if (rest > 0)
           QRB_TRY(apply_qt(A.sub(j0, j0, mk, pw), Tk, nb, A.sub(j0, j0 + pw, mk, rest), ws, st));
       }
+      QRB_TRY(report_progress(h, col0 + nc, st));
     }
     QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
     QRB_CUDA_TRY(cudaEventSynchronize(h->ev1));
@@ -1639,7 +1696,20 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
     }
     return QRB_OK;
   };
-  const int status = body();
+  h->progress = nullptr;
+  int status = QRB_OK;
+  if (progress_host) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, progress_host, 0) != cudaSuccess) {
+      cudaGetLastError();
+      set_last_error("qrb_factorize_host_gated: progress must be page-locked, mapped host memory");
+      status = QRB_EARG;
+    }
+    h->progress = static_cast<int64_t*>(dp);
+  }
+  if (status == QRB_OK) status = body();
+  if (status == QRB_OK && h->progress) status = report_progress(h, h->n, st);
+  h->progress = nullptr;
   if (cs) cudaStreamSynchronize(cs);  // no copy from src may outlive the call
   if (status == QRB_OK) {
     h->factored = true;
@@ -1662,6 +1732,22 @@ int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chu
   if (c1ev) cudaEventDestroy(c1ev);
   if (cs) cudaStreamDestroy(cs);
   return status;
+}
+
+int qrb_factorize_host(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
+                       qrb_report* rep) {
+  return factorize_host_impl(h, src, ld, chunk_cols, nullptr, 0.0, nullptr, rep);
+}
+
+int qrb_factorize_host_gated(qrb_handle* h, const double* src, int64_t ld, int64_t chunk_cols,
+                             const int32_t* ready, double input_gbps, int64_t* progress,
+                             qrb_report* rep) {
+  if (!h || !ready || chunk_cols <= 0 || chunk_cols % h->nb != 0) {
+    clear_report(rep);
+    set_last_error("qrb_factorize_host_gated: need ready flags and chunk_cols a multiple of nb");
+    return QRB_EARG;
+  }
+  return factorize_host_impl(h, src, ld, chunk_cols, ready, input_gbps, progress, rep);
 }
 
 int qrb_get_factors(qrb_handle* h, double* tau, double* T, int64_t ldt) {

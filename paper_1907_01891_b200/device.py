@@ -125,6 +125,15 @@ class QrDevice:
                       "qrb_get_matrix")
         return out
 
+    def get_matrix_async(self, col0: int, ncols: int, dst: np.ndarray, stream_handle: int) -> None:
+        """Columns [col0, col0 + ncols) into the column-major host array dst
+        (m x ncols view, page-locked for a real async copy) on a caller stream,
+        without waiting (qrb_get_matrix_async)."""
+        dst, ld = _host_colmajor(dst)
+        _native.check(self.lib.qrb_get_matrix_async(self._h, int(col0), int(ncols), _ptr(dst), ld,
+                                                    ctypes.c_void_p(stream_handle)),
+                      "qrb_get_matrix_async")
+
     def get_matrix_device(self, t, col0: int = 0) -> None:
         """Copy factored columns [col0, col0 + k) into a torch CUDA tensor of
         shape (k, ld) (column-major m x k, ld >= m), device to device."""
@@ -176,6 +185,29 @@ class QrDevice:
         self.last_report = rep.as_dict()
         return self.last_report
 
+    def factorize_host_gated(self, a, chunk_cols: int, ready: np.ndarray,
+                             input_gbps: float = 0.0, progress: np.ndarray | None = None) -> dict:
+        """factorize_host while another thread is still filling ``a``: chunk c
+        (columns [c*chunk_cols, ...)) is copied once ready[c] > 0 (ready[c] < 0
+        aborts).  ``a`` and ``ready`` must be page-locked (``PinnedHostArray``)
+        for the copies to overlap; the call releases the GIL while it waits.
+        ``progress`` (page-locked int64[1]): kept at the number of leading
+        columns whose factored values are final (stream them out with
+        ``get_matrix_async`` while the call runs)."""
+        a, lda = _host_colmajor(a)
+        if a.shape != (self.m, self.n):
+            raise ValueError(f"matrix must be {self.m}x{self.n}, got {a.shape}")
+        if ready.dtype != np.int32 or ready.size < -(-self.n // chunk_cols):
+            raise ValueError("ready must be an int32 array with one flag per chunk")
+        rep = _native.QrbReport()
+        prog = _ptr(progress) if progress is not None else ctypes.c_void_p(0)
+        _native.check(self.lib.qrb_factorize_host_gated(self._h, _ptr(a), lda, int(chunk_cols),
+                                                        _ptr(ready), float(input_gbps), prog,
+                                                        ctypes.byref(rep)),
+                      "qrb_factorize_host_gated")
+        self.last_report = rep.as_dict()
+        return self.last_report
+
     def solve(self, b, report_block: int | None = None, want_resid: bool = True, out=None):
         """X = R^-1 (Q^T B)[:n] for host B (m x nrhs); returns (X, resid, report).
         ``out`` may be a preallocated (n x nrhs) column-contiguous host array."""
@@ -216,6 +248,34 @@ class QrDevice:
             raise SingularMatrixError(st - 1)
         self.last_report = rep.as_dict()
         return self.last_report
+
+
+class PinnedHostArray:
+    """A numpy array in page-locked host memory (cudaHostRegister on a numpy
+    allocation: exact size -- torch's pinned allocator rounds requests up to a
+    power of two, 64 GB for config 3's 36 GB).  ``.array`` is the array; the
+    registration is dropped by ``close()`` / garbage collection."""
+
+    def __init__(self, shape, dtype=np.float64):
+        import torch
+        self.array = np.empty(shape, dtype=dtype)
+        self._cudart = torch.cuda.cudart()
+        self._ptr = self.array.ctypes.data
+        rc = self._cudart.cudaHostRegister(self._ptr, max(self.array.nbytes, 1), 2)  # Mapped
+        if int(rc) != 0:
+            raise MemoryError(f"cudaHostRegister of {self.array.nbytes} bytes failed ({rc})")
+        self._registered = True
+
+    def close(self) -> None:
+        if getattr(self, "_registered", False):
+            self._cudart.cudaHostUnregister(self._ptr)
+            self._registered = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 def launch_count() -> int:

@@ -23,15 +23,18 @@ reference.  What differs, by design:
 from __future__ import annotations
 
 import csv
+import os
 import io
+import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
 
 from . import dist_api
-from .device import QrDevice
+from .device import PinnedHostArray, QrDevice
 from .errors import (CacheCapacityError, CorruptTileError, MissingFactorsError,
                      SingularMatrixError, TaskIoError)
 from .tile_store import TiledMatrix, TileId
@@ -347,6 +350,141 @@ def _pinned_from_tiles(store: TiledMatrix, rows: int, cols: int):
     return host
 
 
+_STAGE_GBPS = 4.0       # tile read rate the left-/right-looking switch assumes (NVMe class)
+_STAGE_CHUNK = 4096     # columns per gated H2D chunk (qrb_factorize_host's measured best)
+_STAGE_THREADS = int(os.environ.get("QRB_IO_THREADS", "8"))  # tile readers / writers each (the
+# reference has one I/O agent; positional reads and writes parallelise)
+
+
+class _ColumnReader:
+    """Reads the tile column blocks of ``a`` into a page-locked column-major host
+    matrix on a thread pool, in column order, and raises the per-chunk ready
+    flags qrb_factorize_host_gated waits on -- so the first column chunks are
+    already being factored on the GPU while later tiles are still read (the
+    reference overlaps I/O and compute with its one prefetching agent,
+    task_engine.py:330-474).  A failed read marks every pending chunk -1 (the
+    native call then returns instead of waiting) and is re-raised by join()."""
+
+    def __init__(self, a: TiledMatrix, view: np.ndarray, chunk: int, ready: np.ndarray,
+                 threads: int = _STAGE_THREADS):
+        self.a, self.view, self.chunk, self.ready = a, view, chunk, ready
+        self.nblk = a.grid_cols
+        self.done = np.zeros(self.nblk, dtype=bool)
+        self.prefix = 0                      # blocks [0, prefix) are complete
+        self.lock = threading.Lock()
+        self.error: BaseException | None = None
+        self.error_block = 0
+        self.pool = ThreadPoolExecutor(max_workers=max(1, threads))
+        self.futs = []
+        self.seconds = 0.0
+        self.t0 = 0.0
+
+    def _read(self, j: int) -> None:
+        a, b = self.a, self.a.tile_size
+        if self.error is not None:
+            return
+        try:
+            a.read_column_block(j, self.view[:a.rows, j * b:j * b + min(b, a.cols - j * b)])
+        except BaseException as exc:  # noqa: BLE001 -- re-raised in join()
+            with self.lock:
+                if self.error is None:
+                    self.error, self.error_block = exc, j
+                self.ready[self.ready == 0] = -1
+            return
+        with self.lock:
+            self.done[j] = True
+            while self.prefix < self.nblk and self.done[self.prefix]:
+                self.prefix += 1
+            cols = min(a.cols, self.prefix * b)
+            for c in range(len(self.ready)):
+                if self.ready[c] == 0 and (min(a.cols, (c + 1) * self.chunk) <= cols):
+                    self.ready[c] = 1
+
+    def start(self) -> None:
+        self.t0 = time.perf_counter()
+        self.futs = [self.pool.submit(self._read, j) for j in range(self.nblk)]
+
+    def join(self) -> None:
+        for f in self.futs:
+            f.result()
+        self.pool.shutdown(wait=True)
+        self.seconds = time.perf_counter() - self.t0
+        if self.error is not None:
+            raise TaskIoError(self.error_block * self.a.grid_rows, "stage_a",
+                              self.error) from self.error
+
+
+class _ColumnWriter:
+    """Streams the factored matrix into the ``factored`` tile store WHILE the
+    factorization runs: a thread follows the library's progress counter
+    (qrb_factorize_host_gated), copies every tile column block whose columns
+    are final into a ring of page-locked buffers on its own CUDA stream, and
+    hands each to a pool of positional tile writers (the reference's eager
+    write-back agent, task_engine.py:330-474; written once, as there)."""
+
+    def __init__(self, dev: QrDevice, store: TiledMatrix, progress: np.ndarray,
+                 threads: int = _STAGE_THREADS):
+        import torch
+        self.dev, self.store, self.progress = dev, store, progress
+        self.b = store.tile_size
+        self.nblk = store.grid_cols
+        self.lda = (store.rows + 31) // 32 * 32
+        slots = max(2, threads + 2)
+        self.bufs = [PinnedHostArray((self.b, self.lda)) for _ in range(slots)]
+        self.busy = [None] * slots
+        self.pool = ThreadPoolExecutor(max_workers=max(1, threads))
+        self.stream = torch.cuda.Stream(device=dev.device)
+        self.stop = False
+        self.error: BaseException | None = None
+        self.written = 0
+        self.lock = threading.Lock()
+        self.seconds = 0.0
+        self.thread = threading.Thread(target=self._run, daemon=True)
+
+    def _write(self, j: int, slot: int, w: int) -> None:
+        view = self.bufs[slot].array.T[:self.store.rows, :w]      # Fortran (rows x w)
+        n = self.store.write_columns(j * self.b, w, view)
+        with self.lock:
+            self.written += n
+
+    def _run(self) -> None:
+        t0 = time.perf_counter()
+        try:
+            for j in range(self.nblk):
+                w = min(self.b, self.store.cols - j * self.b)
+                while int(self.progress[0]) < j * self.b + w:
+                    if self.stop:
+                        return
+                    time.sleep(0.001)
+                slot = j % len(self.bufs)
+                if self.busy[slot] is not None:
+                    self.busy[slot].result()
+                view = self.bufs[slot].array.T[:self.store.rows, :w]
+                self.dev.get_matrix_async(j * self.b, w, view, self.stream.cuda_stream)
+                self.stream.synchronize()
+                self.busy[slot] = self.pool.submit(self._write, j, slot, w)
+            for f in self.busy:
+                if f is not None:
+                    f.result()
+        except BaseException as exc:  # noqa: BLE001 -- re-raised in join()
+            self.error = exc
+        finally:
+            self.seconds = time.perf_counter() - t0
+
+    def start(self) -> None:
+        self.thread.start()
+
+    def join(self, abort: bool = False) -> None:
+        if abort:
+            self.stop = True
+        self.thread.join()
+        self.pool.shutdown(wait=True)
+        for buf in self.bufs:
+            buf.close()
+        if self.error is not None and not abort:
+            raise TaskIoError(0, "write_factored", self.error) from self.error
+
+
 def _factorize_host_staged(a: TiledMatrix, cfg: EngineConfig, factors_dir: Path,
                            geometry_hash: str) -> tuple["QrFactors", RunReport]:
     from .ooc import HostStagedQR
@@ -408,30 +546,53 @@ def factorize(a: TiledMatrix, config: EngineConfig, factors_dir,
     t_start = time.perf_counter()
     dev = QrDevice(a.rows, a.cols, cfg.panel_width, cfg.device)
     b = a.tile_size
-    t_read = t_h2d = 0.0
-    tiles_read = 0
     trace: list[TaskTrace] = []
     try:
-        for j in range(a.grid_cols):
-            t0 = time.perf_counter()
-            try:
-                blk = a.read_column_block(j)
-            except (OSError, CorruptTileError) as exc:
-                raise TaskIoError(j * a.grid_rows, "stage_a", exc) from exc
-            t1 = time.perf_counter()
-            dev.set_matrix(blk, col0=j * b)
-            t_read += t1 - t0
-            t_h2d += time.perf_counter() - t1
-            tiles_read += a.grid_rows
-        trace.append(TaskTrace(0, "stage_a", 0.0, t_read * 1e3, 0.0))
-        rep = dev.factorize()
-        trace.append(TaskTrace(1, "qr_geqrf_cwy", rep["total_ms"], 0.0, 0.0))
+        # tiles -> page-locked column-major host matrix on reader threads, chunk
+        # by chunk; the GPU copies and factors (left-looking) each chunk as soon
+        # as it is complete, then finishes right-looking (qrb_factorize_host_gated)
+        m, n, nb = a.rows, a.cols, cfg.panel_width
+        lda = (m + 31) // 32 * 32
+        chunk = max(nb, _STAGE_CHUNK // nb * nb)
+        nchunks = -(-n // chunk)
+        host = PinnedHostArray((n, lda))
+        ready = PinnedHostArray((nchunks,), np.int32)
+        ready.array[:] = 0
+        view = host.array.T                                  # (lda, n), Fortran order
+        reader = _ColumnReader(a, view, chunk, ready.array)
         factored = TiledMatrix.create(a.rows, a.cols, b, factors_dir / "factored")
         factors = QrFactors(factored=factored, inner_block=cfg.inner_block, rows=a.rows,
                             cols=a.cols, tile_size=b, panel_width=cfg.panel_width,
                             geometry_hash=geometry_hash, directory=factors_dir)
-        t_write, written = _factor_dir_writes(factors, dev, factors_dir)
-        trace.append(TaskTrace(2, "write_factors", 0.0, 0.0, t_write * 1e3))
+        progress = PinnedHostArray((1,), np.int64)
+        progress.array[0] = 0
+        writer = _ColumnWriter(dev, factored, progress.array)
+        reader.start()
+        writer.start()
+        try:
+            rep = dev.factorize_host_gated(view[:m], chunk, ready.array, input_gbps=_STAGE_GBPS,
+                                           progress=progress.array)
+        except BaseException:
+            writer.join(abort=True)
+            reader.join()                                    # an unreadable tile wins
+            raise
+        reader.join()
+        t_read, t_h2d = reader.seconds, rep["h2d_ms"] / 1e3
+        tiles_read = a.grid_rows * a.grid_cols
+        t0 = time.perf_counter()
+        writer.join()
+        tau, t = dev.factors()
+        tau.astype("<f8").tofile(factors_dir / _TAU_NAME)
+        t.astype("<f8").ravel(order="F").tofile(factors_dir / _T_NAME)
+        t_tail = time.perf_counter() - t0
+        t_write, written = writer.seconds, writer.written
+        host.close()
+        ready.close()
+        progress.close()
+        trace.append(TaskTrace(0, "stage_a_overlapped", 0.0, t_read * 1e3, 0.0))
+        trace.append(TaskTrace(1, "qr_geqrf_cwy", rep["total_ms"], 0.0, 0.0))
+        trace.append(TaskTrace(2, "write_factors_overlapped", 0.0, 0.0, t_write * 1e3))
+        trace.append(TaskTrace(3, "write_tail_after_qr", 0.0, 0.0, t_tail * 1e3))
         factors.save_meta(factors_dir)
     except BaseException:
         dev.close()
