@@ -69,6 +69,27 @@ def panel_home(k: int, nb: int, bw: int, world: int) -> tuple[int, int]:
     return owner_of(blk, world), (blk // world) * bw + (j0 - blk * bw)
 
 
+def owner_chain_sms(mk: int, rest: int, w: int, m_next: int, nb: int, sms: int = 148,
+                    r_min: int = 24, lat_ms: float = 0.25, rate: float = 34.0e9) -> int:
+    """SMs left to the owner's next-block chain while its trailing update (rest
+    columns, K = w, m_k rows) runs capped on the others: the R in
+    {r_min, 32, 48, 64, 96} minimising max(update on sms - R, chain on R).  The
+    chain is ~26 m nb^2 flops of GEMMs per panel pair plus a latency floor; the
+    update 2 m_k w rest flops (rate = flops per ms on all SMs).  Early steps keep
+    r_min (the chain hides under a long update); late steps, where every rank
+    waits for the owner's block, give the chain more."""
+    upd = 2.0 * mk * w * rest / rate                 # ms on all SMs
+    gemm = 26.0 * m_next * nb * nb / rate
+    best_r, best_t = r_min, float("inf")
+    for r in sorted({r_min, 32, 48, 64, 96}):
+        if r < r_min or r >= sms:
+            continue
+        t = max(upd * sms / (sms - r), lat_ms + gemm * sms / r)
+        if t < best_t - 1e-9:
+            best_r, best_t = r, t
+    return best_r
+
+
 class CudaOps:
     """Local arithmetic through the C ABI (stream-ordered qrb_op_* calls on
     torch CUDA tensors holding column-major matrices as (cols, ld) tensors)."""
@@ -131,7 +152,13 @@ class CudaOps:
         if self.world > 1:
             # keep SMs free for the whole owner step: the broadcast's NCCL kernel is
             # launched after the side-stream panel and must not wait for a
-            # persistent full-grid update to drain (the other ranks wait for it)
+            # persistent full-grid update to drain (the other ranks wait for it).
+            # How many: the split minimising the owner's step (its capped update
+            # vs the block chain on the freed SMs) -- late steps, where the chain
+            # is the critical path of every rank, give the chain more SMs
+            g = self.native.get_tuning
+            cap = g("sm_count") - owner_chain_sms(m, rest, w, m_next, nb, g("sm_count"),
+                                                  g("la_sms"), g("la_lat_us") * 1e-3)
             ncap = rest
         if ncap:
             self.native.set_tuning("grid_cap", cap)

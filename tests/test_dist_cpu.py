@@ -172,3 +172,18 @@ def test_config4_memory_plan_at_8_gpus():
     assert not p3["lean_solve"] and p3["fits"]
     # one GPU cannot hold config 4 at all (the host-staged tier takes over)
     assert not qd.memory_plan(270000, 262144, 128, 1, hbm)["fits"]
+
+
+def test_owner_chain_sms_grows_when_the_update_is_short():
+    """The owner's SM split (dist.owner_chain_sms): the look-ahead's 24 SMs while
+    its capped update hides the block chain, more SMs in the late steps where
+    the chain is the critical path of every rank."""
+    from paper_1907_01891_b200.dist import owner_chain_sms
+    # config 3 at 8 GPUs, first step: 8192 local trailing columns, m = 69120
+    assert owner_chain_sms(69120, 8192, 256, 68864, 128) == 24
+    # late step: 1024 local columns left, m_k = 6000 -> chain-bound
+    late = owner_chain_sms(6000, 1024, 256, 5744, 128)
+    assert late > 24
+    # monotone in the remaining update
+    assert owner_chain_sms(20000, 512, 256, 19744, 128) >= owner_chain_sms(20000, 4096, 256,
+                                                                           19744, 128)
