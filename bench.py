@@ -11,9 +11,10 @@ slices/s of the solve is reported beside it.  ``e2e`` repeats a step through
 the public host-buffer API: pinned-host A and B copied in, X and the residual
 norms copied out, all inside the timed region.
 
-``--impl reference`` times the reference algorithm (the oracle restatement of
-oocqr's tiled QR, run on the host cores) on a bounded sample of the same
-workload: the leading 69120 x 1024 column block of the same matrix.
+``--impl reference`` times the reference algorithm on the host cores, like for
+like with our arm's workload: each of the reference's six tile kernels (the
+oracle port of its numpy twin) on the workload's own b = 1024 tiles, the whole
+QR and solve extrapolated as task count x seconds per task.
 
 Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 For N > 1 launch under torchrun (one rank per GPU).
