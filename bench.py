@@ -519,7 +519,10 @@ def ours_arm(args, rank: int, world: int):
         torch.cuda.empty_cache()
 
     # end-to-end through the public host API (pinned host A and B, host X out)
-    a_pin = torch.empty((n, lda), dtype=torch.float64, pin_memory=True)
+    # exact-size page-locked host A (torch's pinned allocator rounds up to a power of two)
+    from paper_1907_01891_b200.device import PinnedHostArray
+    a_pin_hold = PinnedHostArray((n, lda))
+    a_pin = torch.from_numpy(a_pin_hold.array)
     a_pin.copy_(a_dev)
     b_pin = torch.empty((S, ldb), dtype=torch.float64, pin_memory=True)
     b_pin.copy_(b_dev)
@@ -561,6 +564,7 @@ def ours_arm(args, rank: int, world: int):
     del xd, rd
     q.close()
     del a_pin, b_pin, x_pin
+    a_pin_hold.close()
     others = {}
     if args.config == 3 and args.other_configs:
         for c in (1, 2):

@@ -748,7 +748,9 @@ def bench_rank(args, rank: int, world: int):
     # end to end through host buffers: this rank's panels from pinned host memory
     # in, its slice share of X out (factorization + gather + solve inside)
     reset()
-    a_pin = torch.empty(a_local.shape, dtype=torch.float64, pin_memory=True)
+    from .device import PinnedHostArray
+    a_pin_hold = PinnedHostArray(tuple(a_local.shape))      # exact size (no power-of-2 rounding)
+    a_pin = torch.from_numpy(a_pin_hold.array)
     a_pin.copy_(a_local)
     b_pin = torch.empty((max(cnt, 1), lda), dtype=torch.float64, pin_memory=True)
     b_pin.copy_(b_dev)

@@ -339,7 +339,10 @@ def _pinned_from_tiles(store: TiledMatrix, rows: int, cols: int):
     """(n, lda) pinned host tensor (column-major m x n) filled from a tile store."""
     import torch
     lda = (rows + 31) // 32 * 32
-    host = torch.zeros((cols, lda), dtype=torch.float64, pin_memory=True)
+    hold = PinnedHostArray((cols, lda))      # exact size (torch's pinned allocator rounds up)
+    hold.array[:] = 0.0
+    host = torch.from_numpy(hold.array)
+    host._qrb_pinned_hold = hold             # the registration lives as long as the tensor
     view = host.numpy().T            # lda x cols, Fortran
     b = store.tile_size
     for j in range(store.grid_cols):
