@@ -16,7 +16,7 @@ for r in rows:
     if r[0] == "Line No":
         hdr = r
         continue
-    if hdr is None or not r[0].isdigit():
+    if hdr is None or not r[0].isdigit() or len(r) < 8:
         continue
     key = (cur, int(r[0]))
     src[key] = r[1].strip()[:80]
