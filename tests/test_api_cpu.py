@@ -100,3 +100,34 @@ def test_singular_rule_matches_reference_order():
     t = bad_tiles[-1]
     first = next(i for i in range(t * block, (t + 1) * block) if abs(diag[i]) < 1e-300)
     assert first == 19
+
+
+def test_column_reader_flags_chunks_in_order_and_aborts_on_a_bad_tile(tmp_path):
+    """The drop-in factorize's tile reader (task_engine._ColumnReader) raises a
+    chunk's ready flag only once every column of the chunk is in the host
+    matrix, and marks every pending chunk -1 (so the native call returns
+    instead of waiting) when a tile cannot be read."""
+    import numpy as np
+    import paper_1907_01891_b200 as pkg
+    from paper_1907_01891_b200.task_engine import _ColumnReader
+    rng = np.random.default_rng(2)
+    m, n, b = 50, 70, 16
+    a = rng.standard_normal((m, n))
+    t = pkg.TiledMatrix.create(m, n, b, tmp_path / "a")
+    pkg.scatter_matrix(t, a)
+    lda = 64
+    host = np.zeros((n, lda))
+    ready = np.zeros(-(-n // 24), dtype=np.int32)          # chunks of 24 columns
+    r = _ColumnReader(t, host.T, 24, ready, threads=3)
+    r.start()
+    r.join()
+    assert (ready == 1).all()
+    np.testing.assert_array_equal(host.T[:m], a)
+    # a truncated tile: TaskIoError, and no chunk is left waiting
+    t.tile_path(pkg.TileId(1, 2)).write_bytes(b"\0" * 8)
+    ready[:] = 0
+    r = _ColumnReader(t, np.zeros((n, lda)).T, 24, ready, threads=2)
+    r.start()
+    with pytest.raises(pkg.TaskIoError):
+        r.join()
+    assert (ready != 0).all() and (ready == -1).any()
