@@ -180,6 +180,11 @@ QRB_API int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, i
  * time (K = 2nb GEMMs; kernels.py:324-341 applies one inner panel at a time). */
 QRB_API int qrb_get_pair_factors(qrb_handle* h, double* T2, int64_t ldt2);
 
+/* The inverse of qrb_get_pair_factors (after qrb_set_factors): merged pair
+ * reflectors someone already formed -- e.g. the multi-GPU factorization, which
+ * broadcasts one per column block -- so the solve does not merge them again. */
+QRB_API int qrb_set_pair_factors(qrb_handle* h, const double* T2, int64_t ldt2);
+
 /* X = R^-1 (Q^T B)[0:n] for nrhs right-hand sides; resid[j] = ||(Q^T B)[n:m, j]||_2
  * (= ||A x_j - b_j||_2; may be NULL).  B is m x nrhs (ldb), X is n x nrhs (ldx).
  * `on_device` = 1 when B/X/resid are device pointers.  report_block = the tile

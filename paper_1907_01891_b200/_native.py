@@ -84,6 +84,7 @@ SIGNATURES = {
     "qrb_get_matrix_async": (c_int, [c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p]),
     "qrb_get_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_get_pair_factors": (c_int, [c_void_p, c_void_p, c_i64]),
+    "qrb_set_pair_factors": (c_int, [c_void_p, c_void_p, c_i64]),
     "qrb_set_factors": (c_int, [c_void_p, c_void_p, c_void_p, c_i64]),
     "qrb_solve": (c_int, [c_void_p, c_void_p, c_i64, c_i64, c_void_p, c_i64, c_void_p, c_int,
                           c_i64, ctypes.POINTER(QrbReport)]),

@@ -1791,6 +1791,31 @@ int qrb_get_pair_factors(qrb_handle* h, double* T2, int64_t ldt2) {
   return QRB_OK;
 }
 
+int qrb_set_pair_factors(qrb_handle* h, const double* T2, int64_t ldt2) {
+  const int64_t w2 = 2 * int64_t(h ? h->nb : 0);
+  if (!h || !T2 || ldt2 < w2) {
+    set_last_error("qrb_set_pair_factors: bad arguments");
+    return QRB_EARG;
+  }
+  if (!h->factored) {
+    set_last_error("qrb_set_pair_factors: set the factors (qrb_set_factors) first");
+    return QRB_ESTATE;
+  }
+  DeviceGuard g(h->device);
+  const int npairs = h->npanels / 2;
+  if (npairs == 0) return QRB_OK;
+  if (!h->T2 || static_cast<int>(h->t2_valid.size()) != npairs) QRB_TRY(t2_storage(h));
+  for (int p = 0; p < npairs; ++p) {
+    if (!pair_ok(h, 2 * p)) continue;
+    QRB_CUDA_TRY(cudaMemcpy2DAsync(h->T2 + p * w2 * w2, w2 * sizeof(double),
+                                   T2 + int64_t(p) * w2 * ldt2, ldt2 * sizeof(double),
+                                   w2 * sizeof(double), w2, cudaMemcpyDefault, h->stream));
+    h->t2_valid[p] = 1;
+  }
+  QRB_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return QRB_OK;
+}
+
 int qrb_set_factors(qrb_handle* h, const double* tau, const double* T, int64_t ldt) {
   if (!h || !tau || !T || ldt < h->nb) return QRB_EARG;
   DeviceGuard g(h->device);

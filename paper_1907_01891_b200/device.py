@@ -72,6 +72,29 @@ class QrDevice:
         self.npanels = -(-self.n // self.nb)
         self.last_report: dict = {}
 
+    @classmethod
+    def view(cls, t, m: int, n: int, nb: int = 128, device: int = 0) -> "QrDevice":
+        """A handle over the caller's device matrix ``t`` (torch tensor (cols, ld),
+        column-major m x n with ld even, cols >= n), factored / solved in place
+        without a library-owned copy (qrb_create_view); ``t`` is kept alive."""
+        if m < n:
+            raise ValueError(f"matrix must have rows >= cols, got {m}x{n}")
+        ptr, _, cols, ld = colmajor(t)
+        if cols < n or ld < m:
+            raise ValueError(f"view of {cols} x {ld} storage cannot hold a {m} x {n} matrix")
+        self = cls.__new__(cls)
+        self.lib = _native.load()
+        self.m, self.n, self.nb, self.device = int(m), int(n), int(nb), int(device)
+        h = ctypes.c_void_p()
+        _native.check(self.lib.qrb_create_view(self.device, self.m, self.n, self.nb,
+                                                ctypes.c_void_p(ptr), ld, ctypes.byref(h)),
+                      "qrb_create_view")
+        self._h = h
+        self._storage = t
+        self.npanels = -(-self.n // self.nb)
+        self.last_report = {}
+        return self
+
     # -- lifecycle ----------------------------------------------------------
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -164,6 +187,16 @@ class QrDevice:
             raise ValueError("factor shapes do not match this handle")
         _native.check(self.lib.qrb_set_factors(self._h, _ptr(tau), _ptr(t), self.nb),
                       "qrb_set_factors")
+
+    def set_pair_factors(self, t2) -> None:
+        """Merged 2nb x 2nb reflectors of the panel pairs (after set_factors):
+        a torch CUDA tensor (npairs, 2nb, 2nb) -- pair p's block column-major in
+        t2[p] -- so the solve skips merging them (qrb_set_pair_factors)."""
+        w2 = 2 * self.nb
+        if t2.dim() != 3 or tuple(t2.shape[1:]) != (w2, w2) or not t2.is_contiguous():
+            raise ValueError("expected a contiguous (npairs, 2nb, 2nb) tensor")
+        _native.check(self.lib.qrb_set_pair_factors(self._h, ctypes.c_void_p(t2.data_ptr()), w2),
+                      "qrb_set_pair_factors")
 
     # -- compute --------------------------------------------------------------
     def factorize(self) -> dict:

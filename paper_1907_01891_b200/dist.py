@@ -228,6 +228,8 @@ class DistFactors:
     factor_seconds: float = 0.0
     stats: dict = field(default_factory=dict)
     bw: int = 0                         # column block width of the layout (0 = nb)
+    t2_blocks: object = None            # torch (nblocks, 2nb, 2nb): merged reflector of every
+                                        #   panel-pair block, column-major (bw = 2 nb only)
 
     @property
     def block(self) -> int:
@@ -310,8 +312,12 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
         return dist.broadcast(bufs[k % 2][:nelem], src=owner_of(k, world), group=group,
                               async_op=True)
 
-    def unpack(k):  # per-panel T factors (diagonal blocks of T2) and tau
+    t2_blocks = (torch.zeros((nblk, bw, bw), dtype=dt, device=dev) if bw == 2 * nb else None)
+
+    def unpack(k):  # per-panel T factors (diagonal blocks of T2), the block's T2, tau
         j0, w, mk, ldv, nelem, vview, t2view, tauv = views(k)
+        if t2_blocks is not None:
+            t2_blocks[k].copy_(t2view)
         for p in range(-(-w // nb)):
             pw = min(nb, w - p * nb)
             kp = j0 // nb + p
@@ -427,7 +433,8 @@ def factorize_distributed(a_local, m: int, n: int, nb: int, lda: int, rank: int,
     if ev is not None:
         stats["wall_seconds"] = secs
         secs = ev[0].elapsed_time(ev[1]) / 1e3
-    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats, bw)
+    return DistFactors(m, n, nb, lda, rank, world, a_local, t_all, tau_all, secs, stats, bw,
+                       t2_blocks)
 
 
 def gather_factored(f: DistFactors, group=None, place=None):
@@ -457,6 +464,46 @@ def gather_factored(f: DistFactors, group=None, place=None):
         else:
             full[k * f.nb:k * f.nb + pw].copy_(src)
     return full
+
+
+def gather_storage(n: int, bw: int, world: int, lda: int, device):
+    """Device storage for gather_into: (rounds * world * bw, lda) columns."""
+    import torch
+    rounds = -(-(-(-n // bw)) // world)
+    return torch.empty((rounds * world * bw, lda), dtype=torch.float64, device=device)
+
+
+def gather_into(f: DistFactors, out, group=None):
+    """Every rank receives the whole factored matrix straight into ``out``
+    (gather_storage) in global column order: round i all-gathers every
+    rank's i-th local block, and the blocks of round i are the consecutive
+    global blocks i*world .. i*world + world - 1 -- no receive buffer and no
+    reordering copy (gather_factored needs both).  A QrDevice.view over out[:n]
+    then solves without a library-owned copy of the factors."""
+    import torch
+    import torch.distributed as dist
+
+    bw = f.block
+    nblk = -(-f.n // bw)
+    rounds = -(-nblk // f.world)
+    send = torch.zeros((bw, f.lda), dtype=torch.float64, device=f.a_local.device)
+    n_local = f.a_local.shape[0]
+    for i in range(rounds):
+        dst = out[i * f.world * bw:(i + 1) * f.world * bw]
+        c0 = i * bw
+        w = max(0, min(bw, n_local - c0))
+        if f.world == 1:
+            dst[:w].copy_(f.a_local[c0:c0 + w])
+            continue
+        if w == bw:
+            src = f.a_local[c0:c0 + bw]
+        else:                            # a short last block, or none: zero padded
+            send.zero_()
+            if w:
+                send[:w].copy_(f.a_local[c0:c0 + w])
+            src = send
+        dist.all_gather_into_tensor(dst, src, group=group)
+    return out
 
 
 def singular_column(diag: np.ndarray, block: int) -> int:
@@ -664,7 +711,10 @@ def bench_rank(args, rank: int, world: int):
     free, total = torch.cuda.mem_get_info()
     plan = memory_plan(m, n, nb, world, free + 8.0 * a_local.numel(), bw=bw)
     lean = args.lean_solve or plan["lean_solve"]
-    q = None if lean else QrDevice(m, n, nb)
+    # replicated solve: the factors are all-gathered straight into one buffer in
+    # global column order and solved through a handle over it (no second copy)
+    gstore = None if lean else gather_storage(n, bw, world, lda, a_local.device)
+    q = None if lean else QrDevice.view(gstore, m, n, nb, local_rank)
 
     def step():
         reset()
@@ -675,8 +725,10 @@ def bench_rank(args, rank: int, world: int):
             ts = time.perf_counter()
             solve_distributed(f, b_dev[:cnt], ops)
             return f.factor_seconds, 0.0, time.perf_counter() - ts
-        gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
+        gather_into(f, gstore)
         q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+        if f.t2_blocks is not None:
+            q.set_pair_factors(f.t2_blocks)
         t2 = time.perf_counter()
         srep = q.solve_device(b_dev[:cnt], x_dev[:cnt]) if cnt else {"total_ms": 0.0}
         return f.factor_seconds, t2 - t1, srep["total_ms"] / 1e3
@@ -764,8 +816,10 @@ def bench_rank(args, rank: int, world: int):
         xs, _ = solve_distributed(f, b_dev[:cnt], ops)
         x_pin[:cnt].copy_(xs)
     else:
-        gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * nb))
+        gather_into(f, gstore)
         q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+        if f.t2_blocks is not None:
+            q.set_pair_factors(f.t2_blocks)
         if cnt:
             q.solve(b_pin.numpy().T[:m, :cnt], out=x_pin.numpy().T[:, :cnt])
     torch.cuda.synchronize()

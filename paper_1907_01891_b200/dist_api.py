@@ -243,14 +243,17 @@ def solve(factors, b_mat: TiledMatrix, cfg, out_dir: Path, rank: int, world: int
     b_dev = host.to(dev)
     if _replicate is None:
         free = torch.cuda.mem_get_info(dev)[0] if dev.type == "cuda" else 0
-        _replicate = dev.type == "cuda" and 8 * lda * n * 2 < 0.8 * free
+        _replicate = dev.type == "cuda" and 8 * lda * n * 1.1 < 0.8 * free
     t1 = time.perf_counter()
     if _replicate:
         from .device import QrDevice
-        q = QrDevice(m, n, f.nb, dev.index or 0)
+        store = qd.gather_storage(n, f.block, f.world, f.lda, dev)
+        qd.gather_into(f, store)
+        q = QrDevice.view(store, m, n, f.nb, dev.index or 0)
         try:
-            qd.gather_factored(f, place=lambda k, panel: q.set_matrix_device(panel, col0=k * f.nb))
             q.set_factors(f.tau_all.cpu().numpy()[:n], f.t_all.cpu().numpy().T.copy(order="F"))
+            if f.t2_blocks is not None:
+                q.set_pair_factors(f.t2_blocks)
             x = torch.zeros((max(cnt, 1), n + (n & 1)), dtype=torch.float64, device=dev)
             if cnt:
                 q.solve_device(b_dev[:cnt], x[:cnt], report_block=factors.tile_size)

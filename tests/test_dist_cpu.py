@@ -89,6 +89,10 @@ def worker(rank, world, port, m, n, nb, out_dir, lookahead=True, bw=None):
     f = qd.factorize_distributed(a_local, m, n, nb, lda, rank, world, NumpyOps(),
                                  lookahead=lookahead, bw=bw)
     fact = qd.gather_factored(f)
+    # the in-place round-wise gather (global column order, no reorder copy)
+    store = qd.gather_storage(n, f.block, world, lda, a_local.device)
+    qd.gather_into(f, store)
+    assert torch.equal(store[:n], fact), "gather_into differs from gather_factored"
     if rank == 0:
         np.save(os.path.join(out_dir, "factored.npy"), fact[:, :m].numpy().T)
         np.save(os.path.join(out_dir, "t_all.npy"), f.t_all.numpy())

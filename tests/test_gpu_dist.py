@@ -46,6 +46,23 @@ def test_single_rank_nccl_factor_gather_solve():
         x, _, _ = q.solve(bm)
         assert rel_err(x, orc.solve_dense(ref, bm)) <= 1e-8
         q.close()
+        # panel-pair blocks: the factors gathered in place under a view handle, the
+        # broadcast pair reflectors handed to the solve (no second merge, no copy)
+        bw = 2 * nb
+        a2 = qd.scatter_block_cyclic(full, n, bw, 0, 1)
+        f2 = qd.factorize_distributed(a2, m, n, nb, lda, 0, 1, qd.CudaOps(), bw=bw)
+        assert f2.t2_blocks is not None
+        store = qd.gather_storage(n, bw, 1, lda, a2.device)
+        qd.gather_into(f2, store)
+        qv = QrDevice.view(store, m, n, nb)
+        qv.set_factors(f2.tau_all.cpu().numpy()[:n], f2.t_all.cpu().numpy().T.copy(order="F"))
+        x_lazy, _, _ = qv.solve(bm)                       # pairs merged by the solve
+        qv.set_factors(f2.tau_all.cpu().numpy()[:n], f2.t_all.cpu().numpy().T.copy(order="F"))
+        qv.set_pair_factors(f2.t2_blocks)
+        x_given, _, _ = qv.solve(bm)
+        np.testing.assert_array_equal(x_given, x_lazy)
+        assert rel_err(x_given, orc.solve_dense(ref, bm)) <= 1e-8
+        qv.close()
         # memory-lean solve straight from the distributed factors
         bsh = torch.zeros((5, lda), dtype=torch.float64, device="cuda")
         bsh[:, :m] = torch.from_numpy(np.ascontiguousarray(bm.T)).cuda()
