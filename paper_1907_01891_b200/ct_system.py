@@ -99,6 +99,10 @@ CONFIGS = {
     # A = 134885 x 131044, 141 GB -- half of config 4's rows and columns): the
     # host-staged (out-of-HBM) engine's hardware run (profiles/r02_ooc_*)
     7: dict(image=362, views=509, bins=265, slices=16),
+    # the family at 1/4 the width (128 x 128 image, 180 views x 94 bins:
+    # A = 16920 x 16384, m/n = 1.03): the largest instance the reference package
+    # factors here in minutes (tests/golden/make_golden_cfg4q.py)
+    8: dict(image=128, views=180, bins=94, slices=4),
 }
 
 

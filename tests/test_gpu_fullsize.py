@@ -124,17 +124,19 @@ def test_config2_against_reference_golden():
     q.close()
 
 
-def test_reduced_config4_family_against_reference_golden():
-    """Config 4's geometry family at 1/8 width (4230 x 4096, m/n = 1.03): the
-    GPU factorization + solve against the reference package's own result
-    (tests/golden/make_golden_cfg4r.py) -- the parity pin for config 4, whose
-    566 GB the reference cannot factor here."""
+@pytest.mark.parametrize("cfg,fixture", [(6, "ref_ct4r.npz"), (8, "ref_ct4q.npz")])
+def test_reduced_config4_family_against_reference_golden(cfg, fixture):
+    """Config 4's geometry family at 1/8 width (4230 x 4096) and 1/4 width
+    (16920 x 16384), m/n = 1.03 as at full size: the GPU factorization + solve
+    against the reference package's own result (tests/golden/make_golden_cfg4r.py,
+    make_golden_cfg4q.py) -- the parity pin for config 4, whose 566 GB the
+    reference cannot factor here."""
     from pathlib import Path
 
     import torch
     from paper_1907_01891_b200.device import QrDevice
-    ref = np.load(Path(__file__).resolve().parent / "golden" / "ref_ct4r.npz")
-    g = cs.config_geometry(6)
+    ref = np.load(Path(__file__).resolve().parent / "golden" / fixture)
+    g = cs.config_geometry(cfg)
     m, n = g.n_rays, g.n_pixels
     lda = (m + 31) // 32 * 32
     a = cs.densify_device(g, lda)

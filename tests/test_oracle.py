@@ -154,6 +154,26 @@ def test_config2_reference_fixture_inputs():
     assert np.allclose(np.linalg.norm(a @ ref["x"] - b, axis=0), ref["resid"], rtol=1e-12)
 
 
+def test_quarter_width_config4_family_fixture_inputs():
+    """tests/golden/ref_ct4q.npz (the reference package's factorize + solve of
+    config 4's geometry family at 1/4 width, make_golden_cfg4q.py) was made
+    from exactly the matrix and sinograms this repository generates."""
+    import hashlib
+    from pathlib import Path
+
+    from paper_1907_01891_b200 import ct_system as cs
+    ref = np.load(Path(__file__).resolve().parent / "golden" / "ref_ct4q.npz")
+    g = cs.config_geometry(8)
+    assert (g.n_rays, g.n_pixels) == (16920, 16384)
+    assert str(ref["geometry_hash"]) == cs.geometry_hash(g)
+    a = cs.dense_matrix(g, order="C")
+    assert hashlib.sha256(a.tobytes()).hexdigest() == str(ref["a_sha256"])
+    x_true = cs.phantom_stack(8, ref["b"].shape[1])
+    b = cs.noisy_sinograms(a @ x_true, 8)
+    assert np.array_equal(b, ref["b"])
+    assert np.allclose(np.linalg.norm(a @ ref["x"] - b, axis=0), ref["resid"], rtol=1e-12)
+
+
 def test_oracle_matches_reference_on_reduced_config4_family():
     """Config 4's geometry family at 1/8 width (ct_system CONFIGS[6], 4230 x 4096,
     m/n = 1.03 as at full size): the oracle's tiled factorization and solve
