@@ -577,13 +577,24 @@ static int factor_panel_householder(const MatView& panel, double* tau, double* T
 //   factor panel a; apply Q_a^T to panel b's columns; factor panel b;
 //   T = [[T_a, -T_a (V_a^T V_b) T_b], [0, T_b]]   (larft merge)
 // T_a / T_b are also stored per panel (the solve applies nb-wide panels).
-// Panels per outer step (qrb_set_tuning "outer_panels": 1 or 2).
+// Panels per outer step (qrb_set_tuning "outer_panels": 0 = auto, or forced 1, 2
+// or 4).  Auto: single panels for factorizations narrower than "pairs_min_cols"
+// (r02 sweep: config 1, 2160 x 1024, 2.38 -> 2.17 ms; 4230 x 4096 14.85 -> 14.45
+// ms -- the pair's Q_a^T apply and T merge lengthen a chain nothing hides there;
+// config 2, 16384 columns: pairs 209 vs singles 220 ms), pairs / 4-panel blocks
+// otherwise.  The solve always applies merged pairs / quads unless forced to 1.
 static int g_outer_panels = [] {
   const char* e = std::getenv("QRB_OUTER_PANELS");
-  if (!e) return 4;
+  if (!e) return 0;
   const int v = std::atoi(e);
-  return v >= 4 ? 4 : std::max(1, std::min(2, v));
+  return v >= 4 ? 4 : std::max(0, std::min(2, v));
 }();
+static int64_t g_pairs_min_cols = 8192;
+static int outer_panels_for(int64_t n) {
+  if (g_outer_panels > 0) return g_outer_panels;
+  return n < g_pairs_min_cols ? 1 : 4;
+}
+static int outer_panels_solve() { return g_outer_panels > 0 ? g_outer_panels : 4; }
 
 static int factor_panel(const MatView& panel, double* tau, double* T, int64_t ldt, Workspace& ws,
                         cudaStream_t st);
@@ -822,7 +833,7 @@ void invalidate_derived(qrb_handle* h) {
 // merged 2nb-wide reflectors of panel pairs (2p, 2p+1), for the solve's Q^T B
 bool pair_ok(const qrb_handle* h, int k) {
   const int64_t j0 = int64_t(k) * h->nb;
-  return g_outer_panels >= 2 && (k & 1) == 0 && j0 + 2 * int64_t(h->nb) <= h->n &&
+  return outer_panels_solve() >= 2 && (k & 1) == 0 && j0 + 2 * int64_t(h->nb) <= h->n &&
          h->m - j0 >= 2 * int64_t(h->nb);
 }
 
@@ -833,7 +844,7 @@ static int64_t g_t4_min_rhs = 1024;
 // merged 4nb-wide reflectors of panel quads (4q .. 4q+3)
 bool quad_ok(const qrb_handle* h, int k) {
   const int64_t j0 = int64_t(k) * h->nb, w4 = 4 * int64_t(h->nb);
-  return g_outer_panels >= 4 && (k & 3) == 0 && j0 + w4 <= h->n && h->m - j0 >= w4;
+  return outer_panels_solve() >= 4 && (k & 3) == 0 && j0 + w4 <= h->n && h->m - j0 >= w4;
 }
 
 // storage of the merged pair reflectors (npairs blocks of 2nb x 2nb + scratch)
@@ -1055,7 +1066,8 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   const int nb = h->nb;
   const int64_t m = h->m, n = h->n, w2 = 2 * int64_t(nb), blk2 = w2 * w2;
   // outer block = q panels (2: a pair, 4: two pairs merged -> K = 4nb updates)
-  const int q = g_outer_panels >= 4 ? 4 : 2;
+  const int op = outer_panels_for(n);
+  const int q = op >= 4 ? 4 : 2;
   const int64_t wq = q * int64_t(nb), blkq = wq * wq;
   MatView A{h->A, m, n, h->lda};
   auto block_here = [&](int64_t j0, int64_t w) {
@@ -1063,7 +1075,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     // remain (their K = 4nb update pays where the update is long; late steps
     // take pairs, whose shorter panel chain hides better)
     if (w > w2 && n - j0 - w < g_outer4_min_cols) return false;
-    return g_outer_panels >= 2 && j0 + w < n && m - j0 >= w;
+    return op >= 2 && j0 + w < n && m - j0 >= w;
   };
   // merged reflector storage: pairs starting at an even panel are kept for the
   // solve (h->T2); others alternate between two scratch slots
@@ -1667,7 +1679,7 @@ static int factorize_host_impl(qrb_handle* h, const double* src, int64_t ld, int
         const int64_t pw = std::min<int64_t>(nb, h->n - j0), mk = h->m - j0;
         const int k = static_cast<int>(j0 / nb);
         double* Tk = h->T + int64_t(k) * nb * nb;
-        if (g_outer_panels >= 2 && (k & 1) == 0 && j0 + w2 <= col0 + nc && mk >= w2) {
+        if (outer_panels_for(h->n) >= 2 && (k & 1) == 0 && j0 + w2 <= col0 + nc && mk >= w2) {
           double* T2 = nullptr;
           QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2, ws, st,
                                     h->T2 + int64_t(k / 2) * blk2));
@@ -1909,7 +1921,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
                          static_cast<int>(nrhs), h->resid.d(), st));
     g_launches += 1;
   }
-  if (g_outer_panels >= 2) {
+  if (outer_panels_solve() >= 2) {
     QRB_TRY(ensure_rinv2(h));
     QRB_TRY(trsm_upper_h(h, Bv.sub(0, 0, h->n, nrhs), st));
   } else {
@@ -2196,8 +2208,12 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_cholqr_min_rows = value;
     return QRB_OK;
   }
-  if (k == "outer_panels" && (value == 1 || value == 2 || value == 4)) {
+  if (k == "outer_panels" && (value == 0 || value == 1 || value == 2 || value == 4)) {
     g_outer_panels = static_cast<int>(value);
+    return QRB_OK;
+  }
+  if (k == "pairs_min_cols" && value >= 0) {
+    g_pairs_min_cols = value;
     return QRB_OK;
   }
   if (k == "nn_dynamic" && (value == 0 || value == 1)) {
@@ -2246,6 +2262,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "cholqr_min_rows") *value = g_cholqr_min_rows;
   else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
   else if (k == "outer_panels") *value = g_outer_panels;
+  else if (k == "pairs_min_cols") *value = g_pairs_min_cols;
   else if (k == "lookahead") *value = g_lookahead;
   else if (k == "grid_cap") *value = gemm_grid_cap();
   else if (k == "tn_tail") *value = g_tn_tail;

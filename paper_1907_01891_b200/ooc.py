@@ -112,7 +112,7 @@ class _StagedFactors:
             if npairs:
                 _native.check(self.lib.qrb_get_pair_factors(
                     h, _p(self.t2_all, (c0 // w2) * w2 * w2), w2), "qrb_get_pair_factors")
-                pairs_on = _native.get_tuning("outer_panels") >= 2
+                pairs_on = _native.get_tuning("outer_panels") != 1  # 0 = auto: pairs
                 for p in range(npairs):
                     # qrb_api.cu pair_ok: both panels full and 2nb rows below
                     self.pair_valid[c0 // w2 + p] = (pairs_on and (p + 1) * w2 <= w
