@@ -1077,6 +1077,12 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     if (w > w2 && n - j0 - w < g_outer4_min_cols) return false;
     return op >= 2 && j0 + w < n && m - j0 >= w;
   };
+  // width of the block at j0: 4nb / 2nb blocks, or with single panels (op = 1)
+  // nb-wide blocks that still take the look-ahead (the last panel runs serially)
+  auto block_at = [&](int64_t j0) -> int64_t {
+    if (op == 1) return (j0 + nb < n && m - j0 >= nb) ? nb : 0;
+    return block_here(j0, wq) ? wq : block_here(j0, w2) ? w2 : 0;
+  };
   // merged reflector storage: pairs starting at an even panel are kept for the
   // solve (h->T2); others alternate between two scratch slots
   auto t2dst = [&](int64_t j0) -> double* {
@@ -1096,6 +1102,11 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
                           double** Tout) -> int {
     const int64_t mk = m - j0;
     double* Tk = h->T + (j0 / nb) * nb * int64_t(nb);
+    if (w == nb) {  // single panel (T of ld nb)
+      QRB_TRY(factor_panel(A.sub(j0, j0, mk, nb), h->tau + j0, Tk, nb, wsb, sb));
+      *Tout = Tk;
+      return QRB_OK;
+    }
     double* T2a = nullptr;
     QRB_TRY(factor_panel_pair(A, j0, nb, Tk, Tk + int64_t(nb) * nb, h->tau, &T2a, wsb, sb,
                               t2dst(j0)));
@@ -1135,7 +1146,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   while (j0 < n) {
     const int64_t mk = m - j0;
     double* Tk = h->T + (j0 / nb) * nb * int64_t(nb);
-    const int64_t w = have ? have : (block_here(j0, wq) ? wq : block_here(j0, w2) ? w2 : 0);
+    const int64_t w = have ? have : block_at(j0);
     if (w == 0) {
       const int64_t pw = std::min<int64_t>(nb, n - j0);
       QRB_TRY(factor_panel(A.sub(j0, j0, mk, pw), h->tau + j0, Tk, nb, ws, st));
@@ -1152,7 +1163,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     have = 0;
     const int64_t c0 = j0 + w, rest = n - c0;
     const MatView V = A.sub(j0, j0, mk, w);
-    const int64_t wn = block_here(c0, wq) ? wq : block_here(c0, w2) ? w2 : 0;
+    const int64_t wn = block_at(c0);
     bool la = g_lookahead && h->side && wn > 0;
     int64_t ncap = 0;
     if (la) {
@@ -1160,7 +1171,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
       // flops (per pair: 2 Gram + 2 NN per panel, Q_a^T on panel b, the T merge
       // ~ 26 m nb^2; a 4-panel block ~2.3 pairs)
       const double mk1 = static_cast<double>(m - c0);
-      const double pairs = wn == w2 ? 1.0 : 2.3;
+      const double pairs = wn == nb ? 0.45 : wn == w2 ? 1.0 : 2.3;
       const double tp =
           pairs * (g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * R / sms));
       const double capped_rate = rate * (sms - R) / sms;
@@ -1171,6 +1182,9 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
       // r01 sweep, config 2 27.5 -> 28.8 TFLOP/s against skipping short steps);
       // lookahead = 3: only when the remaining NN update outlasts the panel chain
       if (g_lookahead == 3) la = (rest - wn) * per_col / capped_rate > tp;
+      // single panels overlap only on wider matrices (r02: 4230 x 4096 14.46 ->
+      // 13.92 ms with look-ahead; config 1, 2160 x 1024, 2.17 -> 2.20 ms)
+      if (wn == nb && g_lookahead == 1 && n < 2048) la = false;
     }
     if (!la) {
       QRB_TRY(apply_qt(V, TB, w, A.sub(j0, c0, mk, rest), ws, st));

@@ -223,7 +223,7 @@ def test_kernels_actually_launch():
 
 
 @pytest.mark.parametrize("m,n,outer", [(2160, 1024, 2), (3001, 1537, 2), (2160, 1024, 4),
-                                       (3001, 1537, 4)])
+                                       (3001, 1537, 4), (2160, 1024, 1), (3001, 1537, 1)])
 def test_lookahead_factorization_matches_oracle_and_is_deterministic(m, n, outer):
     """Single-GPU look-ahead (qrb_api.cu right_looking): the next panel pair is
     factored on a side stream while the trailing update runs on capped GEMM
