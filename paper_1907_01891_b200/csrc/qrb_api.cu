@@ -581,8 +581,10 @@ static int factor_panel_householder(const MatView& panel, double* tau, double* T
 // or 4).  Auto: single panels for factorizations narrower than "pairs_min_cols"
 // (r02 sweep: config 1, 2160 x 1024, 2.38 -> 2.17 ms; 4230 x 4096 14.85 -> 14.45
 // ms -- the pair's Q_a^T apply and T merge lengthen a chain nothing hides there;
-// config 2, 16384 columns: pairs 209 vs singles 220 ms), pairs / 4-panel blocks
-// otherwise.  The solve always applies merged pairs / quads unless forced to 1.
+// config 2, 16384 columns: pairs 209.3 vs singles 207.7 ms with their look-ahead,
+// but the 64-slice solve after it 7.1 vs 9.6 ms -- pairs keep their merged
+// reflectors for the solve), pairs / 4-panel blocks otherwise.  The solve
+// applies merged pairs / quads where they exist unless forced to 1.
 static int g_outer_panels = [] {
   const char* e = std::getenv("QRB_OUTER_PANELS");
   if (!e) return 0;
@@ -590,6 +592,7 @@ static int g_outer_panels = [] {
   return v >= 4 ? 4 : std::max(0, std::min(2, v));
 }();
 static int64_t g_pairs_min_cols = 8192;
+static int g_tail_singles = 0;  // auto mode: single panels instead of pairs after the 4-panel blocks
 static int outer_panels_for(int64_t n) {
   if (g_outer_panels > 0) return g_outer_panels;
   return n < g_pairs_min_cols ? 1 : 4;
@@ -1080,7 +1083,8 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
   // width of the block at j0: 4nb / 2nb blocks, or with single panels (op = 1)
   // nb-wide blocks that still take the look-ahead (the last panel runs serially)
   auto block_at = [&](int64_t j0) -> int64_t {
-    if (op == 1) return (j0 + nb < n && m - j0 >= nb) ? nb : 0;
+    const bool single = op == 1 || (g_outer_panels == 0 && g_tail_singles && !block_here(j0, wq));
+    if (single) return (j0 + nb < n && m - j0 >= nb) ? nb : 0;
     return block_here(j0, wq) ? wq : block_here(j0, w2) ? w2 : 0;
   };
   // merged reflector storage: pairs starting at an even panel are kept for the
@@ -1900,7 +1904,13 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   QRB_CUDA_TRY(cudaEventRecord(h->ev1, st));
   QRB_TRY(ensure_rinv(h));
-  QRB_TRY(ensure_t2(h, ws));
+  // pair reflectors: those the factorization (or qrb_set_pair_factors) kept are
+  // free; merging the rest pays only for wide right-hand-side batches -- with a
+  // single-panel factorization (config 2) a 64-slice solve applies panels
+  if (static_cast<int>(h->t2_valid.size()) != h->npanels / 2 ||
+      static_cast<int>(h->t4_valid.size()) != h->npanels / 4)
+    QRB_TRY(t2_storage(h));  // factors set without a factorization on this handle
+  if (nrhs >= g_t4_min_rhs) QRB_TRY(ensure_t2(h, ws));
   // quad reflectors: the ones the factorization kept are free; merging the rest
   // (one m_k x 2nb x 2nb product each) pays only for wide right-hand-side
   // batches (config 2, 64 slices: 7.7 -> 9.3 ms with every quad merged per solve)
@@ -1918,7 +1928,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
       k += 4;
       continue;
     }
-    if (pair_ok(h, k)) {  // two panels at once with the merged reflector (K = 2nb)
+    if (pair_ok(h, k) && h->t2_valid[k / 2]) {  // two panels at once (K = 2nb)
       const int64_t w2 = 2 * int64_t(h->nb);
       QRB_TRY(apply_qt(A.sub(j0, j0, mk, w2), h->T2 + int64_t(k / 2) * w2 * w2, w2,
                        Bv.sub(j0, 0, mk, nrhs), ws, st));
@@ -2226,6 +2236,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_outer_panels = static_cast<int>(value);
     return QRB_OK;
   }
+  if (k == "tail_singles" && (value == 0 || value == 1)) {
+    g_tail_singles = static_cast<int>(value);
+    return QRB_OK;
+  }
   if (k == "pairs_min_cols" && value >= 0) {
     g_pairs_min_cols = value;
     return QRB_OK;
@@ -2277,6 +2291,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "nn_dynamic") *value = gemm_nn_dynamic() ? 1 : 0;
   else if (k == "outer_panels") *value = g_outer_panels;
   else if (k == "pairs_min_cols") *value = g_pairs_min_cols;
+  else if (k == "tail_singles") *value = g_tail_singles;
   else if (k == "lookahead") *value = g_lookahead;
   else if (k == "grid_cap") *value = gemm_grid_cap();
   else if (k == "tn_tail") *value = g_tn_tail;

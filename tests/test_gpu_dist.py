@@ -56,10 +56,17 @@ def test_single_rank_nccl_factor_gather_solve():
         qd.gather_into(f2, store)
         qv = QrDevice.view(store, m, n, nb)
         qv.set_factors(f2.tau_all.cpu().numpy()[:n], f2.t_all.cpu().numpy().T.copy(order="F"))
-        x_lazy, _, _ = qv.solve(bm)                       # pairs merged by the solve
-        qv.set_factors(f2.tau_all.cpu().numpy()[:n], f2.t_all.cpu().numpy().T.copy(order="F"))
-        qv.set_pair_factors(f2.t2_blocks)
-        x_given, _, _ = qv.solve(bm)
+        from paper_1907_01891_b200 import _native
+        old_min = _native.get_tuning("t4_min_rhs")
+        _native.set_tuning("t4_min_rhs", 0)               # merge pairs / quads at the solve
+        try:
+            x_lazy, _, _ = qv.solve(bm)                   # pairs merged by the solve
+            qv.set_factors(f2.tau_all.cpu().numpy()[:n],
+                           f2.t_all.cpu().numpy().T.copy(order="F"))
+            qv.set_pair_factors(f2.t2_blocks)
+            x_given, _, _ = qv.solve(bm)                  # pairs as broadcast
+        finally:
+            _native.set_tuning("t4_min_rhs", old_min)
         np.testing.assert_array_equal(x_given, x_lazy)
         assert rel_err(x_given, orc.solve_dense(ref, bm)) <= 1e-8
         qv.close()
