@@ -303,22 +303,27 @@ def cpu_extrapolate(op_s: dict, m: int, n: int, slices: int, b: int) -> dict:
 
 
 def cpu_baseline_run(m: int, n: int, slices: int, coo=None, a_cols=None, steps: int = 1,
-                     warmup: int = 0, b: int = CPU_TILE, w: int = CPU_INNER) -> dict:
+                     warmup: int = 0, b: int = CPU_TILE, w: int = CPU_INNER,
+                     min_seconds: float = 0.0) -> dict:
+    """steps timed executions of the six tile kernels -- more, up to 200, until
+    min_seconds of CPU work have been sampled (the bench's cpu_baseline: ~10 s)."""
     t0, t1 = cpu_tiles(m, n, b, coo, a_cols)
     for _ in range(warmup):
         cpu_op_seconds(t0, t1, b, w)
     runs, wall = [], []
-    for _ in range(steps):
+    while len(runs) < steps or (sum(wall) < min_seconds and len(runs) < 200):
         tic = time.perf_counter()
         runs.append(cpu_op_seconds(t0, t1, b, w))
         wall.append(time.perf_counter() - tic)
+    steps = len(runs)
     op_s = {k: float(np.median([r_[k] for r_ in runs])) for k in runs[0]}
     ex = cpu_extrapolate(op_s, m, n, slices, b)
     ex.update({"op_seconds": op_s, "sample_s_per_step": float(np.mean(wall)), "tile": b,
                "inner_block": w, "cores": len(os.sched_getaffinity(0)),
                "sample": (f"oracle port of oocqr's numpy twin (OOCQR_DISABLE_NUMBA=1 path): one "
                           f"execution of each of the 6 tile kernels on the workload's own b={b} "
-                          f"tiles (w={w}) per step, median over {steps} steps; the {m}x{n} QR and "
+                          f"tiles (w={w}) per step, median over {steps} steps "
+                          f"({sum(wall):.1f} s sampled); the {m}x{n} QR and "
                           f"the {slices}-slice solve EXTRAPOLATED as task count x time per task "
                           f"(grid {-(-m // b)}x{-(-n // b)}, tile I/O excluded, which favours the "
                           f"reference)")})
@@ -570,7 +575,8 @@ def ours_arm(args, rank: int, world: int):
         for c in (1, 2):
             others[f"config{c}"] = measure_config(c)
 
-    cpu = cpu_baseline_run(m, n, S, a_cols=cpu_cols, steps=5, warmup=1, b=min(CPU_TILE, n))
+    cpu = cpu_baseline_run(m, n, S, a_cols=cpu_cols, steps=5, warmup=1, b=min(CPU_TILE, n),
+                           min_seconds=10.0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
