@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -99,6 +100,11 @@ struct Workspace {
   int64_t w2_cols = 0;     // columns / width of the W2 the last apply_qt_w2 formed
   int64_t w2_w = 0;
   uint64_t w2_gen = 0;     // bumped by every apply_qt_w2 (qrb_op_apply_qt_cols checks it)
+  // serialisation of calls that share this workspace (WsUse): one host thread
+  // at a time, and a call on another stream waits for the last call's work
+  std::recursive_mutex mu;
+  cudaEvent_t last_ev = nullptr;
+  cudaStream_t last_st = nullptr;
   void release() {
     Wq.release();
     small.release();
@@ -191,6 +197,39 @@ static Workspace& side_workspace() {
   cudaGetDevice(&dev);
   return ws[dev & 63];
 }
+
+// Entry points of the library share one workspace per device (and a second one
+// for the look-ahead panel).  WsUse makes that safe for several handles and
+// streams: the calling thread holds the workspace for the call, and a call on a
+// different stream than the previous user first waits (on the device) for the
+// previous call's work.  Inside a graph capture no events are used (the
+// captured schedule is replayed on one handle's streams).
+struct WsUse {
+  Workspace& ws;
+  cudaStream_t st;
+  std::lock_guard<std::recursive_mutex> lk;
+  bool active;
+  WsUse(Workspace& w, cudaStream_t s) : ws(w), st(s), lk(w.mu), active(true) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      active = false;
+      return;
+    }
+    if (ws.last_ev && ws.last_st != st) cudaStreamWaitEvent(st, ws.last_ev, 0);
+  }
+  ~WsUse() {
+    if (!active) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();  // joined a capture meanwhile: its work is ordered by the graph
+      return;
+    }
+    if (!ws.last_ev) cudaEventCreateWithFlags(&ws.last_ev, cudaEventDisableTiming);
+    if (ws.last_ev) cudaEventRecord(ws.last_ev, st);
+    ws.last_st = st;
+  }
+};
 
 static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 
@@ -1143,6 +1182,9 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     QRB_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_upd, cudaEventDisableTiming));
     QRB_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pan, cudaEventDisableTiming));
   }
+  // the look-ahead's panel workspace is shared with qrb_op_panel_block(side = 1)
+  std::unique_ptr<WsUse> side_use;
+  if (h->side) side_use.reset(new WsUse(side_workspace(), h->side));
   const double rate = 34.0e9;  // flop per ms of the DMMA update on all SMs (r01 bench)
   double* TB = nullptr;
   int64_t have = 0;  // width of the block at j0 factored by the previous step's look-ahead
@@ -1239,6 +1281,7 @@ static int factorize_graphed(qrb_handle* h, Workspace& ws, cudaStream_t st) {
   const uint64_t epoch = g_graph_epoch.load();
   if (h->fgraph && h->fgraph_epoch == epoch) {
     ++g_graph_replays;
+    WsUse side_use(side_workspace(), st);  // the graph's look-ahead panels use it
     QRB_CUDA_TRY(cudaGraphLaunch(h->fgraph, st));
     g_launches += h->fgraph_launches;
     h->t2_valid = h->fgraph_t2;
@@ -1483,6 +1526,7 @@ int qrb_factorize(qrb_handle* h, qrb_report* rep) {
   h->factored = false;  // until this factorization completes
   invalidate_derived(h);
   Workspace& ws = device_workspace();
+  WsUse use(ws, h->stream);
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = h->stream;
   // non-finite input -> KernelInputError (kernels.py:305-306)
@@ -1597,6 +1641,7 @@ static int factorize_host_impl(qrb_handle* h, const double* src, int64_t ld, int
   h->factored = false;  // A is overwritten from here on
   invalidate_derived(h);
   Workspace& ws = device_workspace();
+  WsUse use(ws, h->stream);
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = h->stream;
   const int nb = h->nb;
@@ -1805,6 +1850,7 @@ int qrb_get_pair_factors(qrb_handle* h, double* T2, int64_t ldt2) {
     return QRB_ESTATE;
   }
   DeviceGuard g(h->device);
+  WsUse use(device_workspace(), h->stream);
   QRB_TRY(ensure_t2(h, device_workspace()));
   const int npairs = h->npanels / 2;
   for (int p = 0; p < npairs; ++p) {
@@ -1893,6 +1939,7 @@ int qrb_solve(qrb_handle* h, const double* B, int64_t ldb, int64_t nrhs, double*
     return static_cast<int>(1 + bad);
   }
   Workspace& ws = device_workspace();
+  WsUse use(ws, h->stream);
   cudaStream_t st = h->stream;
   ProfSession session(h);
   const int64_t ldw = (h->m + 31) & ~int64_t(31);
@@ -1998,7 +2045,9 @@ int qrb_op_panel(double* panel, int64_t ldp, int64_t m, int64_t w, double* tau, 
     return QRB_EARG;
   }
   MatView pv{panel, m, w, ldp};
-  return factor_panel(pv, tau, T, ldt, device_workspace(), static_cast<cudaStream_t>(stream));
+  Workspace& ws = device_workspace();
+  WsUse use(ws, static_cast<cudaStream_t>(stream));
+  return factor_panel(pv, tau, T, ldt, ws, static_cast<cudaStream_t>(stream));
 }
 
 int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const double* T,
@@ -2009,7 +2058,9 @@ int qrb_op_apply_qt(const double* V, int64_t ldv, int64_t m, int64_t w, const do
   }
   MatView Vv{const_cast<double*>(V), m, w, ldv};
   MatView Cv{C, m, nc, ldc};
-  return apply_qt(Vv, T, ldt, Cv, device_workspace(), static_cast<cudaStream_t>(stream));
+  Workspace& ws = device_workspace();
+  WsUse use(ws, static_cast<cudaStream_t>(stream));
+  return apply_qt(Vv, T, ldt, Cv, ws, static_cast<cudaStream_t>(stream));
 }
 
 int qrb_op_gemm_nn_sub(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
@@ -2043,6 +2094,7 @@ int qrb_op_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
                    static_cast<int>(k), 1, mask_a, mask_b, st);
   }
   Workspace& ws = device_workspace();
+  WsUse use(ws, st);
   const int64_t per = ldc * n;
   int used = 0;
   QRB_TRY(ws.Wparts.ensure(sizeof(double) * per * splits, st));
@@ -2064,6 +2116,7 @@ int qrb_op_trsm_upper(const double* R, int64_t ldr, int64_t n, int nb, double* B
   if (n == 0 || nrhs == 0) return QRB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace& ws = device_workspace();
+  WsUse use(ws, st);
   const int nblk = static_cast<int>((n + nb - 1) / nb);
   QRB_TRY(ws.Wparts.ensure(sizeof(double) * nb * nb * nblk, st));
   QRB_TRY(trtri_blocks(R, ldr, static_cast<int>(n), nb, ws.Wparts.d(), st));
@@ -2095,6 +2148,7 @@ int qrb_op_panel_block(double* A, int64_t lda, int64_t m, int64_t w, int nb, dou
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace& ws = side ? side_workspace() : device_workspace();
+  WsUse use(ws, st);
   const MatView Av{A, m, w, lda};
   const int64_t wa = std::min<int64_t>(w, nb), wb = w - wa;
   QRB_TRY(factor_panel(Av.sub(0, 0, m, wa), tau, T, nb, ws, st));
@@ -2120,6 +2174,7 @@ int qrb_op_apply_qt_begin(const double* V, int64_t ldv, int64_t m, int64_t w, co
   }
   if (nc == 0) return QRB_OK;
   Workspace& ws = device_workspace();
+  WsUse use(ws, static_cast<cudaStream_t>(stream));
   QRB_TRY(apply_qt_w2(MatView{const_cast<double*>(V), m, w, ldv}, T, ldt,
                       MatView{const_cast<double*>(C), m, nc, ldc}, ws,
                       static_cast<cudaStream_t>(stream)));
@@ -2134,6 +2189,7 @@ int qrb_op_apply_qt_cols(const double* V, int64_t ldv, int64_t m, int64_t w, dou
     return QRB_EARG;
   }
   Workspace& ws = device_workspace();
+  WsUse use(ws, static_cast<cudaStream_t>(stream));
   if (c_from + ncols > ws.w2_cols || w != ws.w2_w) {
     set_last_error("qrb_op_apply_qt_cols: columns or width beyond the last qrb_op_apply_qt_begin");
     return QRB_EARG;
@@ -2165,6 +2221,7 @@ int qrb_op_apply_qt_td(const double* D, int64_t ldd, int64_t b, int64_t w, const
   if (nc == 0) return QRB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace& ws = device_workspace();
+  WsUse use(ws, st);
   const int64_t ldw = even(w);
   QRB_TRY(ws.W.ensure(sizeof(double) * ldw * nc, st));
   QRB_TRY(ws.W2.ensure(sizeof(double) * ldw * nc, st));

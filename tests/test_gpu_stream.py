@@ -52,3 +52,42 @@ def test_factorize_host_rejects_non_finite():
     with QrDevice(900, 400) as q:
         with pytest.raises(pkg.KernelInputError):
             q.factorize_host(a, chunk_cols=128)
+
+
+def test_two_handles_on_two_streams_from_two_threads():
+    """The per-device workspace shared by every handle (qrb_api.cu WsUse): two
+    handles on different streams, factored and solved concurrently from two
+    host threads, give exactly the results of running them one after the
+    other."""
+    import threading
+
+    import numpy as np
+    import torch
+    from paper_1907_01891_b200.device import QrDevice
+
+    rng = np.random.default_rng(17)
+    mats = [rng.standard_normal((2600, 1300)), rng.standard_normal((3100, 1700))]
+    rhs = [rng.standard_normal((a.shape[0], 4)) for a in mats]
+
+    def run(i, out, stream=None):
+        with QrDevice(*mats[i].shape) as q:
+            if stream is not None:
+                q.set_stream(stream.cuda_stream)
+            q.set_matrix(mats[i])
+            q.factorize()
+            x, _, _ = q.solve(rhs[i])
+            out[i] = (q.get_matrix(), x)
+
+    ref = {}
+    for i in range(2):
+        run(i, ref)
+    got = {}
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ths = [threading.Thread(target=run, args=(i, got, streams[i])) for i in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for i in range(2):
+        np.testing.assert_array_equal(got[i][0], ref[i][0])
+        np.testing.assert_array_equal(got[i][1], ref[i][1])
