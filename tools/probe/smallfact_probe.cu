@@ -208,6 +208,9 @@ int main() {
     for (int i = 1; i < 13; ++i) printf(" %lld", tr[k][i] - tr[k][i - 1]);
     printf("\n");
   }
+  printf("mlu diag (last block) steps 0-8-16-24-end: %lld %lld %lld %lld; l21 row %lld, u12 column %lld\n",
+         tr[1][14] - tr[1][13], tr[1][15] - tr[1][14], tr[1][16] - tr[1][15], tr[1][17] - tr[1][16],
+         tr[1][19] - tr[1][18], tr[1][21] - tr[1][20]);
   printf("chol load %lld  output %lld\n", tr[0][0] - tr[0][31], tr[0][29] - tr[0][30]);
 #endif
   printf("%s (%s)\n", fails ? "FAILURES" : "ALL OK", cudaGetErrorString(cudaGetLastError()));
