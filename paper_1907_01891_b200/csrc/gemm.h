@@ -26,6 +26,8 @@ int gemm_nn_split(const MatView& a_mm, const MatView& b, double* out, int64_t ld
                   cudaStream_t stream, int* used);
 
 int gemm_pick_splits(int M, int N, int K, int max_splits);
+void gemm_set_few_tiles_min_rows(int rows);
+int gemm_few_tiles_min_rows();
 
 // dynamic tile tickets for the persistent NN update (multi-GPU runs, where an
 // NCCL kernel can hold SMs while the update starts); static otherwise

@@ -1114,14 +1114,20 @@ int gemm_sm_count() {
 
 // number of K splits for a long-K (TN) product so that the tile grid fills
 // the machine with little wave quantization
+// rows of K per split when the product has few output tiles ("gram_min_rows")
+static std::atomic<int> g_few_tiles_min_rows{32};  // r02 sweep at config 1: 128 -> 1.96 ms, 64 -> 1.90, 32 -> 1.88
+void gemm_set_few_tiles_min_rows(int rows) { g_few_tiles_min_rows = std::max(16, rows); }
+int gemm_few_tiles_min_rows() { return g_few_tiles_min_rows.load(); }
+
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
   const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
   const int slots = gemm_sm_count();  // one 288-thread CTA per SM (168 regs)
   // few output tiles (the panel's Gram matrices, late trailing updates): one
-  // wave whatever the split, so split as far as >= 128 rows of K per split
-  // allow (r02 trace: the 2160-row Gram ran 7 splits, 21 us)
+  // wave whatever the split, so split as far as gram_min_rows (32) rows of K per
+  // split allow (r02 trace: the 2160-row Gram ran 7 splits, 21 us; 17 splits of
+  // 128 rows 12 us, each CTA 8 us of DMMA work on 34 of the 148 SMs)
   if (tiles * 2 <= slots)
-    return std::max(1, std::min(std::min(max_splits, K / 128), slots / tiles));
+    return std::max(1, std::min(std::min(max_splits, K / g_few_tiles_min_rows.load()), slots / tiles));
   const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
   int best = 1;
   double best_eff = 0.0;
