@@ -24,6 +24,11 @@ int modified_lu_blk(const double* Qt, int ldq, int b, double* Uc, double* NUcS, 
                     double* Ucinv, double* L1invT, double* s, int ldo, int* flag, int bit,
                     cudaStream_t stream);
 
+// which diagonal steps run barrier-free in one warp (bit 0 Cholesky, 1 LU, 2
+// triangular inverse; 7 by default, 0 = the 8-warp barrier versions)
+void smallfact_set_diag(int mask);
+int smallfact_diag();
+
 // C_p = A_p B_p for up to kMax independent products with M, N, K <= 128
 // (column-major, any leading dimensions), one launch
 struct SmallMm {

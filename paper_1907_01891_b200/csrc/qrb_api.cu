@@ -2333,6 +2333,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_la_margin_pct = value;
     return QRB_OK;
   }
+  if (k == "sf_diag" && value >= 0 && value <= 7) {
+    smallfact_set_diag(static_cast<int>(value));
+    return QRB_OK;
+  }
   if (k == "gram_min_rows" && value >= 16 && value <= 4096) {
     gemm_set_few_tiles_min_rows(static_cast<int>(value));
     return QRB_OK;
@@ -2362,6 +2366,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_lat_us") *value = g_la_lat_us;
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
   else if (k == "gram_min_rows") *value = gemm_few_tiles_min_rows();
+  else if (k == "sf_diag") *value = smallfact_diag();
   else if (k == "la_steps") *value = g_la_steps.load();
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
   else if (k == "cholqr_fallbacks") *value = cholqr_fallback_count();

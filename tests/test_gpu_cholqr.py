@@ -20,14 +20,20 @@ def _p(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-@pytest.fixture
-def native():
+@pytest.fixture(params=[7, 0], ids=["warp_diag", "barrier_diag"])
+def native(request):
+    """Every test of this module runs with the 128 x 128 factorizations'
+    diagonal steps in one warp (the default) and as the 8-warp barrier versions
+    (qrb tuning "sf_diag", csrc/smallfact.cu)."""
     from paper_1907_01891_b200 import _native
     lib = _native.load()
     algo, rows = _native.get_tuning("panel_algo"), _native.get_tuning("cholqr_min_rows")
+    diag = _native.get_tuning("sf_diag")
+    _native.set_tuning("sf_diag", request.param)
     yield _native, lib
     _native.set_tuning("panel_algo", algo)
     _native.set_tuning("cholqr_min_rows", rows)
+    _native.set_tuning("sf_diag", diag)
 
 
 def _panel(lib, a_np, algo, native_mod):
