@@ -20,10 +20,11 @@ def _p(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-@pytest.fixture(params=[7, 0], ids=["warp_diag", "barrier_diag"])
+@pytest.fixture(params=[31, 7, 0], ids=["warp_diag4", "warp_diag", "barrier_diag"])
 def native(request):
     """Every test of this module runs with the 128 x 128 factorizations'
-    diagonal steps in one warp (the default) and as the 8-warp barrier versions
+    diagonal steps shared by four warps (Cholesky, LU; the default), all in one
+    warp, and as the 8-warp barrier versions
     (qrb tuning "sf_diag", csrc/smallfact.cu)."""
     from paper_1907_01891_b200 import _native
     lib = _native.load()
