@@ -1114,6 +1114,11 @@ int gemm_sm_count() {
 
 // number of K splits for a long-K (TN) product so that the tile grid fills
 // the machine with little wave quantization
+// 128 x 32 tiles for NN products with few 128 x 64 tiles ("few_tiles_bn32")
+static std::atomic<int> g_few_tiles_bn32{1};
+void gemm_set_few_tiles_bn32(int on) { g_few_tiles_bn32 = on != 0; }
+int gemm_few_tiles_bn32() { return g_few_tiles_bn32.load(); }
+
 // rows of K per split when the product has few output tiles ("gram_min_rows")
 static std::atomic<int> g_few_tiles_min_rows{32};  // r02 sweep at config 1: 128 -> 1.96 ms, 64 -> 1.90, 32 -> 1.88
 void gemm_set_few_tiles_min_rows(int rows) { g_few_tiles_min_rows = std::max(16, rows); }
@@ -1180,6 +1185,14 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
     set_last_error("gemm_nn: output must be 16-byte aligned with even ld");
     return QRB_ERR_ARG;
   }
+  // few tiles and a short K (the trailing update of a small matrix: 16 x 4 tiles
+  // of 8 us at m = 2160): 128 x 32 tiles, one per CTA, put twice as many SMs to
+  // work; C - acc is rounded once either way, so the result is bitwise the
+  // persistent kernel's (uncapped launches only: a capped launch must stay on
+  // its SMs)
+  if (epi == GEMM_EPI_SUB && g_few_tiles_bn32.load() && gemm_grid_cap() == 0 && N > 32 &&
+      K <= 512 && ((M + BM - 1) / BM) * ((N + 63) / 64) * 2 <= gemm_sm_count())
+    return launch<false, 32, GEMM_EPI_SUB>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
   static const bool asyncepi = std::getenv("QRB_NN_SYNC_EPI") == nullptr;
   if (epi == GEMM_EPI_SUB && asyncepi && !(std::getenv("QRB_NN_STAGED_C")) &&
       !(std::getenv("QRB_NN_CLASSIC"))) {
@@ -1299,6 +1312,15 @@ int gemm_nn(const MatView& a_mm, const MatView& b, double* out, int64_t ldo, int
       QRB_CUDA_TRY(cudaGetLastError());
       return QRB_OK;
     }
+  }
+  {
+    // few tiles (a short panel's Q1 = P R1^-1: 17 x 2 tiles of 8 us at m = 2160):
+    // 128 x 32 tiles put twice as many SMs to work; same K order per element, so
+    // the result is bitwise the 128 x 64 kernel's
+    const int num_m = (M + BM - 1) / BM;
+    if (g_few_tiles_bn32.load() && N > 32 && num_m * ((N + 63) / 64) * 2 <= gemm_sm_count())
+      return launch<false, 32, GEMM_EPI_STORE>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0,
+                                               stream);
   }
   return launch<false, 64, GEMM_EPI_STORE>(a_mm, b, out, ldo, 0, M, N, K, 1, mask_a, 0, stream);
 }

@@ -2337,6 +2337,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     smallfact_set_diag(static_cast<int>(value));
     return QRB_OK;
   }
+  if (k == "few_tiles_bn32" && value >= 0 && value <= 1) {
+    gemm_set_few_tiles_bn32(static_cast<int>(value));
+    return QRB_OK;
+  }
   if (k == "gram_min_rows" && value >= 16 && value <= 4096) {
     gemm_set_few_tiles_min_rows(static_cast<int>(value));
     return QRB_OK;
@@ -2366,6 +2370,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_lat_us") *value = g_la_lat_us;
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
   else if (k == "gram_min_rows") *value = gemm_few_tiles_min_rows();
+  else if (k == "few_tiles_bn32") *value = gemm_few_tiles_bn32();
   else if (k == "sf_diag") *value = smallfact_diag();
   else if (k == "la_steps") *value = g_la_steps.load();
   else if (k == "cholqr_panels") *value = g_cholqr_panels.load();
