@@ -2333,7 +2333,7 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_la_margin_pct = value;
     return QRB_OK;
   }
-  if (k == "sf_diag" && value >= 0 && value <= 31) {
+  if (k == "sf_diag" && value >= 0 && value <= 63) {
     smallfact_set_diag(static_cast<int>(value));
     return QRB_OK;
   }
