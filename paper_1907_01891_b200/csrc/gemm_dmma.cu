@@ -1115,14 +1115,19 @@ int gemm_sm_count() {
 // number of K splits for a long-K (TN) product so that the tile grid fills
 // the machine with little wave quantization
 // 128 x 32 tiles for NN products with few 128 x 64 tiles ("few_tiles_bn32")
-static std::atomic<int> g_few_tiles_bn32{1};
-void gemm_set_few_tiles_bn32(int on) { g_few_tiles_bn32 = on != 0; }
+static std::atomic<int> g_few_tiles_bn32{2};
+void gemm_set_few_tiles_bn32(int on) { g_few_tiles_bn32 = on; }  // 1: NN products, 2: + split TN
 int gemm_few_tiles_bn32() { return g_few_tiles_bn32.load(); }
 
 // rows of K per split when the product has few output tiles ("gram_min_rows")
 static std::atomic<int> g_few_tiles_min_rows{32};  // r02 sweep at config 1: 128 -> 1.96 ms, 64 -> 1.90, 32 -> 1.88
 void gemm_set_few_tiles_min_rows(int rows) { g_few_tiles_min_rows = std::max(16, rows); }
 int gemm_few_tiles_min_rows() { return g_few_tiles_min_rows.load(); }
+
+static bool few_tiles_tn32(int M, int N) {
+  return g_few_tiles_bn32.load() > 1 && N > 32 &&
+         ((M + BM - 1) / BM) * ((N + 63) / 64) * 2 <= gemm_sm_count();
+}
 
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
   const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
@@ -1131,8 +1136,12 @@ int gemm_pick_splits(int M, int N, int K, int max_splits) {
   // wave whatever the split, so split as far as gram_min_rows (32) rows of K per
   // split allow (r02 trace: the 2160-row Gram ran 7 splits, 21 us; 17 splits of
   // 128 rows 12 us, each CTA 8 us of DMMA work on 34 of the 148 SMs)
-  if (tiles * 2 <= slots)
-    return std::max(1, std::min(std::min(max_splits, K / g_few_tiles_min_rows.load()), slots / tiles));
+  if (tiles * 2 <= slots) {
+    // the TN launch then runs 128 x 32 tiles (few_tiles_tn32): half the partial
+    // output per CTA to store and to reduce, twice the K per split
+    const int t = few_tiles_tn32(M, N) ? ((M + BM - 1) / BM) * ((N + 31) / 32) : tiles;
+    return std::max(1, std::min(std::min(max_splits, K / g_few_tiles_min_rows.load()), slots / t));
+  }
   const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
   int best = 1;
   double best_eff = 0.0;
@@ -1161,6 +1170,9 @@ int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ld
                   cudaStream_t stream, int* used) {
   *used = 0;
   if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
+  if (splits > 1 && gemm_grid_cap() == 0 && few_tiles_tn32(M, N))
+    return launch<true, 32, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,
+                                            mask_a, mask_b, stream, used);
   return launch<true, 64, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,
                                           mask_a, mask_b, stream, used);
 }

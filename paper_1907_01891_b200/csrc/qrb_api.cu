@@ -2337,7 +2337,7 @@ int qrb_set_tuning(const char* key, int64_t value) {
     smallfact_set_diag(static_cast<int>(value));
     return QRB_OK;
   }
-  if (k == "few_tiles_bn32" && value >= 0 && value <= 1) {
+  if (k == "few_tiles_bn32" && value >= 0 && value <= 2) {
     gemm_set_few_tiles_bn32(static_cast<int>(value));
     return QRB_OK;
   }
