@@ -41,6 +41,10 @@ struct SmallMm {
 struct SmallMmBatch {
   static constexpr int kMax = 4;
   SmallMm p[kMax];
+  // inside a stream capture: the launch also sets the graph conditional `cond`
+  // to (*cond_flag != 0) (saves the one-thread kernel that would do it)
+  cudaGraphConditionalHandle cond;
+  const int* cond_flag;  // nullptr: no conditional to set
 };
 int small_mm_batch(const SmallMmBatch& batch, int count, cudaStream_t stream);
 

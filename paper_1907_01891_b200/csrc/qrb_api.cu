@@ -469,17 +469,25 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
     QRB_TRY(small_mm_batch(bt, 2, st));
   }
   QRB_TRY(modified_lu(Qt, LD, b, Uc, NUcS, L1, Uci, L1iT, s, LD, flag, 4, st));
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  cudaGraph_t cg = nullptr;
+  QRB_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, nullptr, nullptr));
+  cudaGraphConditionalHandle hc{};
   {
     SmallMmBatch bt{};
     bt.p[0] = SmallMm{R2i, Uci, M, LD, LD, LD, b, b, b};
     bt.p[1] = SmallMm{NUcS, L1iT, Tt, LD, LD, LD, b, b, b};
+    if (cst == cudaStreamCaptureStatusActive) {
+      // captured: the flag is final here (every kernel that raises it precedes
+      // this launch), so this launch also sets the IF node's condition
+      QRB_CUDA_TRY(cudaGraphConditionalHandleCreate(&hc, cg, 0, 0));
+      bt.cond = hc;
+      bt.cond_flag = flag;
+    }
     QRB_TRY(small_mm_batch(bt, 2, st));
   }
   g_launches += 8;
   ++g_cholqr_panels;
-  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
-  cudaGraph_t cg = nullptr;
-  QRB_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, nullptr, nullptr));
   auto finish = [&](cudaStream_t s2) -> int {
     // V below the top block: L2 = Q1[b:] R2^-1 Uc^-1 = Q1[b:] M, written over P[b:]
     if (m > b)
@@ -492,10 +500,6 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
   if (cst == cudaStreamCaptureStatusActive) {
     // captured (qrb_factorize graph): an IF/ELSE node on the flag -- the
     // branch not taken costs nothing at replay
-    cudaGraphConditionalHandle hc;
-    QRB_CUDA_TRY(cudaGraphConditionalHandleCreate(&hc, cg, 0, 0));
-    QRB_TRY(set_conditional_from_flag(hc, flag, st));
-    g_launches += 1;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
     QRB_CUDA_TRY(cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, &deps, &ndeps));
