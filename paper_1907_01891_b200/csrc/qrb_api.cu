@@ -396,15 +396,31 @@ static int64_t g_cholqr_min_rows = 1024;  // CholeskyQR2 wins from ~2k rows up (
 static std::atomic<int64_t> g_cholqr_panels{0};
 
 // a non-blocking stream per device for capturing conditional-node bodies
-static cudaStream_t capture_helper_stream() {
-  static cudaStream_t hs[64] = {nullptr};
+static cudaStream_t capture_helper_stream(int which = 0) {
+  static cudaStream_t hs[2][64] = {{nullptr}};
   static std::mutex mu;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  if (!hs[dev & 63] && cudaStreamCreateWithFlags(&hs[dev & 63], cudaStreamNonBlocking) != cudaSuccess)
-    hs[dev & 63] = nullptr;
-  return hs[dev & 63];
+  cudaStream_t& s = hs[which & 1][dev & 63];
+  if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+  return s;
+}
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return QRB_OK;
+  set_last_error(std::string("CUDA: ") + cudaGetErrorString(e));
+  return QRB_ERR_CUDA;
+}
+// fork / join events for two independent kernels inside a captured IF body
+static cudaEvent_t capture_helper_event(int which) {
+  static cudaEvent_t ev[2][64] = {{nullptr}};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaEvent_t& e = ev[which & 1][dev & 63];
+  if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+  return e;
 }
 
 // Householder QR of the panel column by column (the path for short panels and
@@ -524,7 +540,25 @@ static int factor_panel_cholqr2(const MatView& panel, double* tau, double* T, in
         rc = cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, T, ldt, flag, hs);
         if (rc == QRB_OK) rc = factor_panel_householder(panel, tau, T, ldt, ws, hs);
       } else {
-        rc = finish(hs);
+        // V below the top block and the top block / tau / T are independent:
+        // two parallel nodes of the body (fork and join by events)
+        cudaStream_t hs2 = capture_helper_stream(1);
+        cudaEvent_t ef = capture_helper_event(0), ej = capture_helper_event(1);
+        if (m > b && hs2 && ef && ej) {
+          rc = cuda_status(cudaEventRecord(ef, hs));
+          if (rc == QRB_OK) rc = cuda_status(cudaStreamWaitEvent(hs2, ef, 0));
+          if (rc == QRB_OK)
+            rc = cholqr_write_top(panel.ptr, panel.ld, b, R, s, L1, Tt, LD, tau, LD, T, ldt, flag,
+                                  hs2);
+          if (rc == QRB_OK) rc = cuda_status(cudaEventRecord(ej, hs2));
+          if (rc == QRB_OK)
+            rc = gemm_nn(MatView{Wq + b, m - b, b, mw}, MatView{M, b, b, LD}, panel.ptr + b,
+                         panel.ld, m - b, b, b, GEMM_EPI_STORE, 0, hs);
+          if (rc == QRB_OK) rc = cuda_status(cudaStreamWaitEvent(hs, ej, 0));
+          g_launches += 2;
+        } else {
+          rc = finish(hs);
+        }
       }
       cudaGraph_t body = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(hs, &body);
