@@ -469,7 +469,10 @@ def ours_arm(args, rank: int, world: int):
         roofline["nn_parts"] = {
             "full_grid": {"achieved": ua, "frac": ua / FP64_PEAK_TFLOPS,
                           "launches": uk["launches"], "ms": uk["ms"]},
+            # (chain-bound late steps leave the chain up to la_sms_max SMs, so a few
+            # capped launches had fewer SMs than this: frac_of_its_sms is a lower bound)
             "capped": {"achieved": ca, "sms": sms - la_sms,
+                       "sms_min": sms - max(la_sms, native.get_tuning("la_sms_max")),
                        "frac_of_its_sms": ca / (FP64_PEAK_TFLOPS * (sms - la_sms) / sms),
                        "launches": ck["launches"], "ms": ck["ms"]}}
     shares = {k: round(v["ms"] / sum(x["ms"] for x in kstats.values()), 4) for k, v in kstats.items()}

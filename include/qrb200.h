@@ -302,8 +302,14 @@ QRB_API int qrb_release_workspace(void);
  *                      capped GEMM grids, pair s+1 is factored on a second (high-priority)
  *                      stream on the remaining SMs; 0: serial; 3: only when the update
  *                      outlasts the modelled panel time.  Results are bitwise identical.
- *   "la_sms"           SMs left to the look-ahead panel (default 24)
+ *   "la_sms"           SMs left to the look-ahead panel (default 16)
+ *   "la_sms_max"       in chain-bound steps (the whole remaining update shorter than the
+ *                      modelled chain) the chain is left more SMs, up to this many (72),
+ *                      until the two balance
  *   "la_lat_us", "la_margin_pct"  panel-time model sizing the capped part of the update
+ *                      (450 us per pair + its GEMM flops on the chain's SMs; +10%)
+ *   "few_tiles_bn32"   2 (default): NN products and split TN products with few 128 x 64
+ *                      tiles run 128 x 32 tiles (twice the CTAs); 1: NN only; 0: off
  *   "la_steps"         (read only) steps that ran with look-ahead
  *   "grid_cap"         CTAs of the GEMMs launched by the calling host thread (0 = no cap)
  *   "sf_diag"          bit mask, 31 by default: the 32-wide diagonal steps of the 128 x 128

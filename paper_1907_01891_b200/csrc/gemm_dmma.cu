@@ -1124,9 +1124,13 @@ static std::atomic<int> g_few_tiles_min_rows{32};  // r02 sweep at config 1: 128
 void gemm_set_few_tiles_min_rows(int rows) { g_few_tiles_min_rows = std::max(16, rows); }
 int gemm_few_tiles_min_rows() { return g_few_tiles_min_rows.load(); }
 
-static bool few_tiles_tn32(int M, int N) {
-  return g_few_tiles_bn32.load() > 1 && N > 32 &&
-         ((M + BM - 1) / BM) * ((N + 63) / 64) * 2 <= gemm_sm_count();
+// ... and a short K per CTA (<= 256 rows with 128 x 64 tiles): in a long main
+// loop the 128 x 64 tile's operand reuse matters more than the epilogue (the
+// 256-slice solve's W = V^T B, K = m_k / 9, lost 5% with 128 x 32 tiles)
+static bool few_tiles_tn32(int M, int N, int K) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
+  return g_few_tiles_bn32.load() > 1 && N > 32 && tiles * 2 <= gemm_sm_count() &&
+         static_cast<int64_t>(K) * tiles <= 256 * static_cast<int64_t>(gemm_sm_count());
 }
 
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
@@ -1139,7 +1143,7 @@ int gemm_pick_splits(int M, int N, int K, int max_splits) {
   if (tiles * 2 <= slots) {
     // the TN launch then runs 128 x 32 tiles (few_tiles_tn32): half the partial
     // output per CTA to store and to reduce, twice the K per split
-    const int t = few_tiles_tn32(M, N) ? ((M + BM - 1) / BM) * ((N + 31) / 32) : tiles;
+    const int t = few_tiles_tn32(M, N, K) ? ((M + BM - 1) / BM) * ((N + 31) / 32) : tiles;
     return std::max(1, std::min(std::min(max_splits, K / g_few_tiles_min_rows.load()), slots / t));
   }
   const int kmax = std::max(1, K / 256);  // keep >= 256 rows of K per split
@@ -1170,7 +1174,7 @@ int gemm_tn_split(const MatView& a_km, const MatView& b, double* out, int64_t ld
                   cudaStream_t stream, int* used) {
   *used = 0;
   if (M <= 0 || N <= 0 || K <= 0) return QRB_OK;
-  if (splits > 1 && gemm_grid_cap() == 0 && few_tiles_tn32(M, N))
+  if (splits > 1 && gemm_grid_cap() == 0 && few_tiles_tn32(M, N, K))
     return launch<true, 32, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,
                                             mask_a, mask_b, stream, used);
   return launch<true, 64, GEMM_EPI_STORE>(a_km, b, out, ldo, split_stride, M, N, K, splits,

@@ -1118,9 +1118,10 @@ static int g_lookahead = [] {
   const char* e = std::getenv("QRB_LOOKAHEAD");
   return e ? std::atoi(e) : 1;
 }();
-static int g_la_sms = 24;              // SMs left to the look-ahead panel (r01 sweep: 8..48)
-static int64_t g_la_lat_us = 250;      // latency part of a pair's panel chain (r01 sweep)
-static int64_t g_la_margin_pct = 25;   // capped window = (1 + margin) x modelled panel time
+static int g_la_sms = 16;              // SMs left to the look-ahead panel (r01 sweep: 8..48)
+static int64_t g_la_lat_us = 450;      // latency part of a pair's panel chain (r01 sweep)
+static int64_t g_la_margin_pct = 10;   // capped window = (1 + margin) x modelled panel time
+static int64_t g_la_sms_max = 72;      // chain-bound steps may leave the chain up to this many SMs
 static std::atomic<int64_t> g_la_steps{0};
 // outer_panels = 4 (default): 4-panel blocks while >= 24576 trailing columns
 // remain, pairs after (r01 sweep at config 3: pairs only 34.49, 4-panel blocks
@@ -1250,16 +1251,27 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     const int64_t wn = block_at(c0);
     bool la = g_lookahead && h->side && wn > 0;
     int64_t ncap = 0;
+    int Rs = R;  // SMs left to the chain in this step
     if (la) {
       // modelled chain time of the next block on R SMs: latency part + its GEMM
       // flops (per pair: 2 Gram + 2 NN per panel, Q_a^T on panel b, the T merge
       // ~ 26 m nb^2; a 4-panel block ~2.3 pairs)
       const double mk1 = static_cast<double>(m - c0);
       const double pairs = wn == nb ? 0.45 : wn == w2 ? 1.0 : 2.3;
-      const double tp =
-          pairs * (g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * R / sms));
-      const double capped_rate = rate * (sms - R) / sms;
       const double per_col = 2.0 * static_cast<double>(mk) * w;  // NN flops per column
+      auto chain_ms = [&](int r) {
+        return pairs * (g_la_lat_us * 1e-3 + 26.0 * mk1 * nb * nb / (rate * r / sms));
+      };
+      // chain-bound steps (the whole capped update is shorter than the chain on
+      // R SMs: the second half of a config-2-sized factorization): leave the
+      // chain more SMs, up to "la_sms_max", until the two balance
+      Rs = R;
+      if (g_la_sms_max > R)
+        while (Rs + 8 <= std::min<int64_t>(g_la_sms_max, sms / 2 + 22) &&
+               chain_ms(Rs) > (rest - wn) * per_col / (rate * (sms - Rs) / sms))
+          Rs += 8;
+      const double tp = chain_ms(Rs);
+      const double capped_rate = rate * (sms - Rs) / sms;
       const double want = (1.0 + g_la_margin_pct / 100.0) * tp * capped_rate / per_col;
       ncap = std::min<int64_t>(rest - wn, (static_cast<int64_t>(want) + 63) / 64 * 64);
       // lookahead = 1: always (even a short update hides part of the panel:
@@ -1283,7 +1295,7 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
     QRB_TRY(apply_qt_nn(V, C, 0, wn, ws, st));
     QRB_CUDA_TRY(cudaEventRecord(h->ev_upd, st));
     {
-      GemmGridCap cap(sms - R);
+      GemmGridCap cap(sms - Rs);
       QRB_TRY(apply_qt_nn(V, C, wn, ncap, ws, st, QRB_K_GEMM_NN_CAP));
     }
     QRB_TRY(apply_qt_nn(V, C, wn + ncap, rest - wn - ncap, ws, st));
@@ -2367,6 +2379,10 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_la_lat_us = value;
     return QRB_OK;
   }
+  if (k == "la_sms_max" && value >= 0 && value <= 120) {
+    g_la_sms_max = value;
+    return QRB_OK;
+  }
   if (k == "la_margin_pct" && value >= 0 && value <= 1000) {
     g_la_margin_pct = value;
     return QRB_OK;
@@ -2407,6 +2423,7 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_sms") *value = g_la_sms;
   else if (k == "la_lat_us") *value = g_la_lat_us;
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
+  else if (k == "la_sms_max") *value = g_la_sms_max;
   else if (k == "gram_min_rows") *value = gemm_few_tiles_min_rows();
   else if (k == "few_tiles_bn32") *value = gemm_few_tiles_bn32();
   else if (k == "sf_diag") *value = smallfact_diag();
