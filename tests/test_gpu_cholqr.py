@@ -20,7 +20,7 @@ def _p(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-@pytest.fixture(params=[31, 7, 0], ids=["warp_diag4", "warp_diag", "barrier_diag"])
+@pytest.fixture(params=[63, 7, 0], ids=["warp_diag4", "warp_diag", "barrier_diag"])
 def native(request):
     """Every test of this module runs with the 128 x 128 factorizations'
     diagonal steps shared by four warps (Cholesky, LU; the default), all in one

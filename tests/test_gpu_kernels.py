@@ -56,6 +56,30 @@ def test_gemm_nn_sub(m, n, k):
     assert rel_err(to_host(Ct, m), C - A @ B) <= 1e-13
 
 
+@pytest.mark.parametrize("m,n,k", [(2160, 256, 128), (2032, 896, 128), (1000, 130, 256), (300, 70, 37)])
+def test_gemm_nn_sub_few_tiles_128x32_is_bitwise_the_128x64_result(m, n, k):
+    """Updates with few 128 x 64 tiles run 128 x 32 tiles (qrb tuning
+    "few_tiles_bn32", csrc/gemm_dmma.cu): same K order per element and C - acc
+    rounded once either way, so the two kernels agree bit for bit."""
+    from paper_1907_01891_b200 import _native
+    rng = np.random.default_rng(m * 7 + n + k)
+    A, B, C = (rng.standard_normal(s) for s in [(m, k), (k, n), (m, n)])
+    At, lda = to_dev(A)
+    Bt, ldb = to_dev(B)
+    keep = _native.get_tuning("few_tiles_bn32")
+    out = []
+    try:
+        for knob in (0, 2):
+            _native.set_tuning("few_tiles_bn32", knob)
+            Ct, ldc = to_dev(C)
+            assert lib().qrb_op_gemm_nn_sub(P(At), lda, P(Bt), ldb, P(Ct), ldc, m, n, k, None) == 0
+            out.append(to_host(Ct, m))
+    finally:
+        _native.set_tuning("few_tiles_bn32", keep)
+    np.testing.assert_array_equal(out[0], out[1])
+    assert rel_err(out[1], C - A @ B) <= 1e-13
+
+
 @pytest.mark.parametrize("k,m,n,splits", [(4616, 128, 5, 1), (4616, 128, 5, 18), (5000, 40, 70, 3),
                                           (48, 128, 128, 4), (1000, 128, 1000, 2), (17, 3, 2, 1)])
 @pytest.mark.parametrize("mask_a,mask_b", [(0, 0), (1, 0), (1, 1)])
