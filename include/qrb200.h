@@ -312,12 +312,12 @@ QRB_API int qrb_release_workspace(void);
  *                      tiles run 128 x 32 tiles (twice the CTAs); 1: NN only; 0: off
  *   "la_steps"         (read only) steps that ran with look-ahead
  *   "grid_cap"         CTAs of the GEMMs launched by the calling host thread (0 = no cap)
- *   "sf_diag"          bit mask, 31 by default: the 32-wide diagonal steps of the 128 x 128
+ *   "sf_diag"          bit mask, 63 by default: the 32-wide diagonal steps of the 128 x 128
  *                      Cholesky (1) / modified LU (2) / triangular inverses (4) of the
  *                      CholeskyQR2 panel run barrier-free in one warp; Cholesky (8) / LU
- *                      (16) with four warps sharing the rows (win over 1 / 2); 0: the
- *                      8-warp one-barrier-per-column versions (initial value from
- *                      QRB_SF_DIAG)
+ *                      (16) with four warps sharing the rows (win over 1 / 2); 32: the
+ *                      batched 128^3 products on 16 CTAs each; 0: the 8-warp
+ *                      one-barrier-per-column versions (initial value from QRB_SF_DIAG)
  *   "gram_min_rows"    rows of K per CTA when a product has few output tiles (a panel's
  *                      Gram matrices): 32 by default
  *   "sm_count"         (read only) SMs of the current device
