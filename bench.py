@@ -461,6 +461,10 @@ def ours_arm(args, rank: int, world: int):
         ck, uk = kstats["gemm_nn_capped"], kstats["gemm_nn"]
         sms = torch.cuda.get_device_properties(0).multi_processor_count
         la_sms = native.get_tuning("la_sms")
+        if m >= native.get_tuning("la_tall_rows"):
+            # tall steps (>= la_tall_rows rows: nearly all of the capped time at this
+            # size) leave the chain la_sms_tall SMs
+            la_sms = max(la_sms, native.get_tuning("la_sms_tall"))
         ca = ck["flops"] / (ck["ms"] * 1e-3) / 1e12
         ua = uk["flops"] / (uk["ms"] * 1e-3) / 1e12
         # NN's two launch kinds: whole-GPU rate of the full-grid launches, and the

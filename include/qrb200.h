@@ -302,7 +302,8 @@ QRB_API int qrb_release_workspace(void);
  *                      capped GEMM grids, pair s+1 is factored on a second (high-priority)
  *                      stream on the remaining SMs; 0: serial; 3: only when the update
  *                      outlasts the modelled panel time.  Results are bitwise identical.
- *   "la_sms"           SMs left to the look-ahead panel (default 16)
+ *   "la_sms"           SMs left to the look-ahead panel (default 16; "la_sms_tall", also 16
+ *                      by default, in steps with at least "la_tall_rows" = 32768 rows)
  *   "la_sms_max"       in chain-bound steps (the whole remaining update shorter than the
  *                      modelled chain) the chain is left more SMs, up to this many (72),
  *                      until the two balance

@@ -1122,6 +1122,8 @@ static int g_la_sms = 16;              // SMs left to the look-ahead panel (r01 
 static int64_t g_la_lat_us = 450;      // latency part of a pair's panel chain (r01 sweep)
 static int64_t g_la_margin_pct = 10;   // capped window = (1 + margin) x modelled panel time
 static int64_t g_la_sms_max = 72;      // chain-bound steps may leave the chain up to this many SMs
+static int64_t g_la_sms_tall = 16;     // SMs left to the chain in steps with >= g_la_tall_rows rows (24: cleaner overlap, -0.15% at config 3)
+static int64_t g_la_tall_rows = 32768;
 static std::atomic<int64_t> g_la_steps{0};
 // outer_panels = 4 (default): 4-panel blocks while >= 24576 trailing columns
 // remain, pairs after (r01 sweep at config 3: pairs only 34.49, 4-panel blocks
@@ -1265,8 +1267,14 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
       // chain-bound steps (the whole capped update is shorter than the chain on
       // R SMs: the second half of a config-2-sized factorization): leave the
       // chain more SMs, up to "la_sms_max", until the two balance
-      Rs = R;
-      if (g_la_sms_max > R)
+      // tall steps: the chain's GEMM part grows with the rows (7.4 ms per pair on
+      // 16 SMs at m = 69120, 13.9 ms on 8), and a chain that outlasts its capped
+      // window contends with the full-grid launches that follow; from
+      // "la_tall_rows" rows on it gets "la_sms_tall" SMs
+      Rs = mk1 >= static_cast<double>(g_la_tall_rows)
+               ? std::max<int>(R, static_cast<int>(std::min<int64_t>(g_la_sms_tall, sms / 2)))
+               : R;
+      if (g_la_sms_max > Rs)
         while (Rs + 8 <= std::min<int64_t>(g_la_sms_max, sms / 2 + 22) &&
                chain_ms(Rs) > (rest - wn) * per_col / (rate * (sms - Rs) / sms))
           Rs += 8;
@@ -2379,6 +2387,14 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_la_lat_us = value;
     return QRB_OK;
   }
+  if (k == "la_sms_tall" && value >= 0 && value <= 100) {
+    g_la_sms_tall = value;
+    return QRB_OK;
+  }
+  if (k == "la_tall_rows" && value >= 0) {
+    g_la_tall_rows = value;
+    return QRB_OK;
+  }
   if (k == "la_sms_max" && value >= 0 && value <= 120) {
     g_la_sms_max = value;
     return QRB_OK;
@@ -2424,6 +2440,8 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_lat_us") *value = g_la_lat_us;
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
   else if (k == "la_sms_max") *value = g_la_sms_max;
+  else if (k == "la_sms_tall") *value = g_la_sms_tall;
+  else if (k == "la_tall_rows") *value = g_la_tall_rows;
   else if (k == "gram_min_rows") *value = gemm_few_tiles_min_rows();
   else if (k == "few_tiles_bn32") *value = gemm_few_tiles_bn32();
   else if (k == "sf_diag") *value = smallfact_diag();

@@ -157,8 +157,10 @@ class CudaOps:
             # vs the block chain on the freed SMs) -- late steps, where the chain
             # is the critical path of every rank, give the chain more SMs
             g = self.native.get_tuning
+            # (at least 24: the single-GPU default la_sms is 8, but here the
+            # broadcast's NCCL CTAs share the freed SMs with the chain)
             cap = g("sm_count") - owner_chain_sms(m, rest, w, m_next, nb, g("sm_count"),
-                                                  g("la_sms"), g("la_lat_us") * 1e-3)
+                                                  max(24, g("la_sms")), g("la_lat_us") * 1e-3)
             ncap = rest
         if ncap:
             self.native.set_tuning("grid_cap", cap)
