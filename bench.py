@@ -693,6 +693,15 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (torch.distributed) path even at N=1")
     args = ap.parse_args()
+    if args.gpus > 1 and args.impl == "ours" and args.dist_backend == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            # one rank per GPU over NCCL: fail before starting ranks that cannot get a device
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {have} "
+                  "(--dist-backend gloo runs the multi-rank path with ranks sharing a GPU)",
+                  file=sys.stderr)
+            sys.exit(2)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without a launcher: start N ranks (one per
         # GPU) under torch.distributed.run on this node; rank 0 prints the line
