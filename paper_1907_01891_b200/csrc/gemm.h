@@ -26,6 +26,7 @@ int gemm_nn_split(const MatView& a_mm, const MatView& b, double* out, int64_t ld
                   cudaStream_t stream, int* used);
 
 int gemm_pick_splits(int M, int N, int K, int max_splits);
+int gemm_tn_split_tiles(int M, int N, int K);
 void gemm_set_few_tiles_bn32(int on);
 int gemm_few_tiles_bn32();
 void gemm_set_few_tiles_min_rows(int rows);

@@ -1133,6 +1133,12 @@ static bool few_tiles_tn32(int M, int N, int K) {
          static_cast<int64_t>(K) * tiles <= 256 * static_cast<int64_t>(gemm_sm_count());
 }
 
+// output tiles of a split TN launch of this shape (128 x 32 tiles when the
+// few-tile rule applies, 128 x 64 otherwise)
+int gemm_tn_split_tiles(int M, int N, int K) {
+  return ((M + BM - 1) / BM) * (few_tiles_tn32(M, N, K) ? (N + 31) / 32 : (N + 63) / 64);
+}
+
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
   const int tiles = ((M + BM - 1) / BM) * ((N + 63) / 64);
   const int slots = gemm_sm_count();  // one 288-thread CTA per SM (168 regs)

@@ -236,8 +236,8 @@ static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 // K splits for a product whose output has only a few 128 x 64 tiles (the solve's
 // T^T W and R_kk^-1 Y_k with 256 right-hand sides: 8 tiles on 148 SMs); a
 // function of the shape only, so results are deterministic
-static int small_splits(int M, int N, int K) {
-  const int tiles = ((M + 127) / 128) * ((N + 63) / 64);
+static int small_splits(int M, int N, int K, bool tn = false) {
+  const int tiles = tn ? gemm_tn_split_tiles(M, N, K) : ((M + 127) / 128) * ((N + 63) / 64);
   int s = 1;
   while (tiles * s * 2 <= gemm_sm_count() && K / (s * 2) >= 32 && s < 16) s *= 2;
   return s;
@@ -339,7 +339,7 @@ static int apply_qt_w2(const MatView& V, const double* T, int64_t ldt, const Mat
   {
     ProfScope ps(QRB_K_GEMM_TT, 2.0 * w * static_cast<double>(w) * nc,
                  8.0 * (2.0 * w * nc + (double)w * w), st);
-    const int s2 = small_splits(w, nc, w);
+    const int s2 = small_splits(w, nc, w, true);
     if (s2 > 1) {
       QRB_TRY(small_product(true, Tv, Wv, ws.W2.d(), ldw, w, nc, w, s2, ws, st));
     } else {
