@@ -311,6 +311,10 @@ QRB_API int qrb_release_workspace(void);
  *                      (450 us per pair + its GEMM flops on the chain's SMs; +10%)
  *   "few_tiles_bn32"   2 (default): NN products and split TN products with few 128 x 64
  *                      tiles run 128 x 32 tiles (twice the CTAs); 1: NN only; 0: off
+ *   "early_singles"    1 (default): factorizations of single panels narrower than 2048
+ *                      columns apply each update in two pieces (the next panel's columns
+ *                      first) and start the next panel beside the second, which leaves it
+ *                      "early_sms" (8) SMs; same arithmetic with and without look-ahead
  *   "la_steps"         (read only) steps that ran with look-ahead
  *   "grid_cap"         CTAs of the GEMMs launched by the calling host thread (0 = no cap)
  *   "sf_diag"          bit mask, 63 by default: the 32-wide diagonal steps of the 128 x 128

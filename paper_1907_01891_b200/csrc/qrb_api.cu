@@ -1122,6 +1122,8 @@ static int g_la_sms = 16;              // SMs left to the look-ahead panel (r01 
 static int64_t g_la_lat_us = 450;      // latency part of a pair's panel chain (r01 sweep)
 static int64_t g_la_margin_pct = 10;   // capped window = (1 + margin) x modelled panel time
 static int64_t g_la_sms_max = 72;      // chain-bound steps may leave the chain up to this many SMs
+static int g_early_singles = 1;        // "early_singles": two-piece update of narrow single-panel factorizations
+static int64_t g_early_sms = 8;        // SMs its second piece leaves to the chain (0: none reserved; sweep 0..32: 1.492, 1.482 at 4-16)
 static int64_t g_la_sms_tall = 16;     // SMs left to the chain in steps with >= g_la_tall_rows rows (24: cleaner overlap, -0.15% at config 3)
 static int64_t g_la_tall_rows = 32768;
 static std::atomic<int64_t> g_la_steps{0};
@@ -1289,6 +1291,34 @@ static int right_looking(qrb_handle* h, int64_t col0, Workspace& ws, cudaStream_
       // single panels overlap only on wider matrices (r02: 4230 x 4096 14.46 ->
       // 13.92 ms with look-ahead; config 1, 2160 x 1024, 2.17 -> 2.20 ms)
       if (wn == nb && g_lookahead == 1 && n < 2048) la = false;
+    }
+    // Narrow factorizations of single panels (config 1: 2160 x 1024): the update
+    // is too short to hide anything behind its NN part alone, so it is applied in
+    // two complete pieces -- the next panel's columns first (TN + T^T + NN on nb
+    // columns), then the rest -- and the next panel's chain starts after the
+    // first piece, beside the second.  The two-piece arithmetic is used with and
+    // without look-ahead (the split-K of a piece depends on its width), so the
+    // factors stay bitwise identical between the two.
+    if (g_early_singles && wn == nb && w == nb && n < 2048 && rest > wn) {
+      const MatView C = A.sub(j0, c0, mk, rest);
+      QRB_TRY(apply_qt(V, TB, w, C.sub(0, 0, mk, wn), ws, st));
+      const bool ov = g_lookahead && h->side;
+      if (ov) QRB_CUDA_TRY(cudaEventRecord(h->ev_upd, st));
+      {
+        // (beside the chain the second piece leaves it "early_sms" SMs)
+        GemmGridCap cap(ov && g_early_sms > 0 ? sms - static_cast<int>(g_early_sms) : gemm_grid_cap());
+        QRB_TRY(apply_qt(V, TB, w, C.sub(0, wn, mk, rest - wn), ws, st));
+      }
+      if (ov) {
+        ++g_la_steps;
+        QRB_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_upd, 0));
+        QRB_TRY(factor_block(c0, static_cast<int>(wn), side_workspace(), h->side, &TB));
+        QRB_CUDA_TRY(cudaEventRecord(h->ev_pan, h->side));
+        QRB_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_pan, 0));
+        have = wn;
+      }
+      j0 = c0;
+      continue;
     }
     if (!la) {
       QRB_TRY(apply_qt(V, TB, w, A.sub(j0, c0, mk, rest), ws, st));
@@ -2387,6 +2417,14 @@ int qrb_set_tuning(const char* key, int64_t value) {
     g_la_lat_us = value;
     return QRB_OK;
   }
+  if (k == "early_sms" && value >= 0 && value <= 64) {
+    g_early_sms = value;
+    return QRB_OK;
+  }
+  if (k == "early_singles" && value >= 0 && value <= 1) {
+    g_early_singles = static_cast<int>(value);
+    return QRB_OK;
+  }
   if (k == "la_sms_tall" && value >= 0 && value <= 100) {
     g_la_sms_tall = value;
     return QRB_OK;
@@ -2441,6 +2479,8 @@ int qrb_get_tuning(const char* key, int64_t* value) {
   else if (k == "la_margin_pct") *value = g_la_margin_pct;
   else if (k == "la_sms_max") *value = g_la_sms_max;
   else if (k == "la_sms_tall") *value = g_la_sms_tall;
+  else if (k == "early_singles") *value = g_early_singles;
+  else if (k == "early_sms") *value = g_early_sms;
   else if (k == "la_tall_rows") *value = g_la_tall_rows;
   else if (k == "gram_min_rows") *value = gemm_few_tiles_min_rows();
   else if (k == "few_tiles_bn32") *value = gemm_few_tiles_bn32();
